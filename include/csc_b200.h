@@ -1,0 +1,172 @@
+/*
+ * csc_b200.h — C ABI of the B200-native compressive-spectral-clustering hot path.
+ *
+ * The reference (`cscluster`, pure Python + scipy) has no C API: its hot path is
+ * reached through Python seams.  Each entry point below replaces
+ * one of those seams; the reference interface it stands in for is cited as
+ * file:line relative to the reference package `pkg/src/cscluster/`.
+ *
+ * Conventions
+ *  - Every call returns an int status: CSC_OK (0) or one of CSC_ERR_*.  The
+ *    message of the last failure on the calling thread is csc_last_error().
+ *    Python maps CSC_ERR_INVALID -> ValueError, CSC_ERR_GRAPH -> GraphError
+ *    (a ValueError subclass, graph.py:19-20), anything else -> RuntimeError.
+ *  - Buffers are plain pointers.  Each data pointer may be host memory
+ *    (pageable or pinned) or device memory of the graph's device; the library
+ *    detects which with cudaPointerGetAttributes and stages host buffers.
+ *  - Dense blocks are row-major (one node's columns contiguous) with a leading
+ *    dimension `ld` (elements), like the reference's C-contiguous N x w numpy
+ *    arrays (spectrum.py:84, features.py:63).  `io_dtype` gives the element type
+ *    of those buffers (CSC_F64 / CSC_F32); the arithmetic runs in the graph's
+ *    compute dtype.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    stream-ordered; a call returns after its results are in the caller's
+ *    buffers for host outputs, and asynchronously for device outputs.
+ *  - Graph handles are immutable after creation and may be shared between
+ *    threads and streams (LaplacianOp is immutable/reentrant, graph.py:128-134).
+ */
+#ifndef CSC_B200_H
+#define CSC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSC_ABI_VERSION 1
+
+/* status codes */
+#define CSC_OK 0
+#define CSC_ERR_INVALID 1 /* bad argument / shape  -> ValueError                 */
+#define CSC_ERR_GRAPH 2   /* bad edge data         -> GraphError (graph.py:19)    */
+#define CSC_ERR_CUDA 3    /* CUDA runtime failure or no device -> RuntimeError    */
+#define CSC_ERR_NOMEM 4   /* device allocation failed -> MemoryError              */
+
+/* element / compute types */
+#define CSC_F64 0
+#define CSC_F32 1
+
+/* build flags */
+#define CSC_SELF_LOOPS_ERROR 0 /* build_graph(self_loops="error"), graph.py:115-118 */
+#define CSC_SELF_LOOPS_DROP 1  /* build_graph(self_loops="drop"),  graph.py:119-120 */
+
+typedef struct csc_graph csc_graph;
+
+/* ---- library ------------------------------------------------------------ */
+int csc_abi_version(void);
+const char* csc_last_error(void);
+/* Number of CUDA kernels this library has launched in the process so far. */
+int csc_launch_count(int64_t* out);
+/* Tuning knobs (process-wide; not to be changed while calls are in flight):
+ *   "panel_width"   columns per panel (0 = auto)      "recurrence"  0 Clenshaw, 1 forward
+ *   "cache_hints"   1 streaming hints on, 0 off        "block_threads" threads per CTA
+ *   "profile"       1 = time the Chebyshev step kernels with CUDA events            */
+int csc_set_option(const char* key, int64_t value);
+int csc_get_option(const char* key, int64_t* value);
+/* Profile counters of the Chebyshev step kernels since the last reset:
+ * total device ms, launches, algorithmic bytes (SURVEY.md §8d formula applied to
+ * the streams each launch touches). */
+int csc_profile_read(double* step_ms, int64_t* step_launches, double* step_bytes);
+int csc_profile_reset(void);
+
+/* ---- graph (K1) --------------------------------------------------------- */
+/* Canonical CSR -> device normalized operator.  Replaces laplacian_op
+ * (graph.py:164-169) over a Graph (graph.py:23-55): degrees are fp64 row sums
+ * (graph.py:63), d^-1/2 is 0 for zero degree (graph.py:168), and the stored
+ * operator is Wn = D^-1/2 W D^-1/2 in the compute dtype.  indptr/indices/weights
+ * must already be canonical (sorted, no duplicates, no zeros); they are
+ * validated (CSC_ERR_GRAPH otherwise). */
+int csc_graph_create(int64_t num_nodes, int64_t nnz, const int32_t* indptr, const int32_t* indices,
+                     const double* weights, int dtype, int device, void* stream, csc_graph** out);
+
+/* Edge triples -> canonical CSR on the device, then as csc_graph_create.
+ * Replaces build_graph (graph.py:73-125) after its host-side validation:
+ * per-direction duplicates summed (graph.py:122-123), W = max(A, A^T)
+ * (graph.py:124), sorted columns, explicit zeros dropped (graph.py:60-62). */
+int csc_graph_build_coo(int64_t num_nodes, int64_t num_edges, const int64_t* src, const int64_t* dst,
+                        const double* weights, int self_loops, int dtype, int device, void* stream,
+                        csc_graph** out);
+
+int csc_graph_destroy(csc_graph* g);
+
+/* Sizes of a handle. */
+int csc_graph_info(const csc_graph* g, int64_t* num_nodes, int64_t* nnz, int* dtype, int* device);
+
+/* Copy the canonical CSR and degrees back (any pointer may be NULL).  Gives the
+ * Graph dataclass fields indptr/indices/weights/degrees (graph.py:31-35) and the
+ * operator's d_inv_sqrt (graph.py:137). */
+int csc_graph_export(const csc_graph* g, int32_t* indptr, int32_t* indices, double* weights,
+                     double* degrees, double* d_inv_sqrt, void* stream);
+
+/* ---- operator / filter (K2) --------------------------------------------- */
+/* Y = L X for an N x ncols block.  Replaces LaplacianOp.apply (graph.py:147-155). */
+int csc_laplacian_apply(const csc_graph* g, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                        int ncols, int io_dtype, void* stream);
+
+/* Y = sum_l c_l T_l(L - I) X, l = 0..ncoeffs-1 (ncoeffs = order + 1).
+ * Replaces apply_filter (filters.py:140-155). */
+int csc_cheb_filter(const csc_graph* g, const double* coeffs, int ncoeffs, const void* X, int64_t ldx,
+                    void* Y, int64_t ldy, int ncols, int io_dtype, void* stream);
+
+/* count = sum over all entries of (h(L) R)^2, accumulated in fp64; the filtered
+ * block is never written.  Replaces the filter + reduction of eigencount
+ * (spectrum.py:81-86). */
+int csc_eigencount(const csc_graph* g, const double* coeffs, int ncoeffs, const void* R, int64_t ldr,
+                   int ncols, int io_dtype, double* count, void* stream);
+
+/* F = rownormalize(h(L) R).  Rows whose norm is <= 1e-300 are left zero and
+ * flagged in zero_flags[N] (uint8, may be NULL); *num_zero receives their count.
+ * Replaces build_features (features.py:70-93, norm rule at :80-87). */
+int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, const void* R, int64_t ldr,
+                       int ncols, int io_dtype, void* F, int64_t ldf, uint8_t* zero_flags, int64_t* num_zero,
+                       void* stream);
+
+/* Column-sharded features (each rank owns a slice of the signal columns):
+ * Y = h(L) R plus rowsq[i] = sum_c Y[i,c]^2 over this slice (fp64, host or
+ * device).  After the caller sums rowsq over the slices (NCCL all-reduce),
+ * csc_normalize_rows divides by the global row norm with the zero-row rule of
+ * features.py:80-87.  One rank with all columns equals csc_build_features. */
+int csc_filter_rowsq(const csc_graph* g, const double* coeffs, int ncoeffs, const void* R, int64_t ldr, int ncols,
+                     int io_dtype, void* Y, int64_t ldy, double* rowsq, void* stream);
+int csc_normalize_rows(const void* Y, int64_t ldy, int64_t num_rows, int ncols, int io_dtype, const double* rowsq,
+                       void* F, int64_t ldf, uint8_t* zero_flags, int64_t* num_zero, int device, void* stream);
+
+/* AP = mask * X + gamma * (g(L) X + ridge * X) for an N x ncols block, with the
+ * high-pass g given by hp_coeffs and mask[N] a uint8 sampling mask (host or
+ * device).  Replaces _system_apply (sampling.py:119-121). */
+int csc_system_apply(const csc_graph* g, const double* hp_coeffs, int ncoeffs, double gamma, double ridge,
+                     const uint8_t* mask, const void* X, int64_t ldx, void* AP, int64_t ldap, int ncols,
+                     int io_dtype, void* stream);
+
+/* ---- sampling / interpolation / assignment (K4-K6) ------------------------ */
+/* out[i, :] = F[idx[i], :] for i < n.  Replaces feats.rows[sampling.indices]
+ * (pipeline.py:176) and SamplingSet.restrict (sampling.py:52-54). */
+int csc_gather_rows(const void* F, int64_t ldf, int64_t num_rows, int ncols, int io_dtype,
+                    const int64_t* idx, int64_t n, void* out, int64_t ldo, int device, void* stream);
+
+/* Blocked per-column CG on (M^T M + gamma (g(L) + ridge I)) X = M^T C, with the
+ * matched high-pass g given by hp_coeffs.  reduced is n x k row-major fp64 (host
+ * or device).  X_out is N x k (io_dtype, leading dim ldx).  Per-column outputs
+ * (host or device, may be NULL): iterations (int64[k]), residuals (fp64[k]),
+ * converged (uint8[k]); *iters_run receives the number of CG iterations run.
+ * Replaces interpolate_all (sampling.py:124-180) with _system_apply
+ * (sampling.py:119-121). */
+int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int ncoeffs, double gamma, double ridge,
+                 const int64_t* sample_idx, int64_t n, const double* reduced, int k, double tol,
+                 int64_t max_iters, void* X_out, int64_t ldx, int io_dtype, int64_t* iterations,
+                 double* residuals, uint8_t* converged, int64_t* iters_run, void* stream);
+
+/* labels[i] = argmax_j soft[i, j] / ||soft[:, j]|| (ties -> lowest j, zero-norm
+ * columns never win); rows that are identically zero fall back to the raw argmax
+ * (= 0) and are flagged in fallback[N] (may be NULL); *num_fallback receives
+ * their count.  CSC_ERR_INVALID when every column is zero.  Replaces assign
+ * (sampling.py:197-220). */
+int csc_assign(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dtype, int64_t* labels,
+               uint8_t* fallback, int64_t* num_fallback, int device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSC_B200_H */

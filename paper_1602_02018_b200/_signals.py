@@ -1,0 +1,74 @@
+"""Host-side random signal blocks, drawn by numpy exactly as the reference draws them.
+
+Parity requires the reference's seeded numpy streams, so
+signals are generated on the host.  Two things make that cheaper without
+changing a single value:
+
+- blocks are written into page-locked (pinned) buffers with
+  ``rng.standard_normal(out=...)`` and scaled in place, so the device copy runs
+  at full PCIe/C2C rate and no temporary is allocated;
+- ``ProbeStream`` draws the next eigencount probe block on a worker thread while
+  the GPU filters the current one.  The probe stream is lambda-independent
+  (spectrum.py:84), so the i-th block is the same whatever the dichotomy does.
+"""
+
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """numpy array in page-locked memory when a CUDA torch is available, else plain."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            t = torch.empty(tuple(int(s) for s in shape), dtype=torch.float64 if np.dtype(dtype) == np.float64
+                            else torch.float32, pin_memory=True)
+            return t.numpy()  # the array's base keeps the pinned tensor alive
+    except Exception:
+        pass
+    return np.empty(shape, dtype=dtype)
+
+
+def normal_block(rng: np.random.Generator, n: int, w: int, out: np.ndarray | None = None) -> np.ndarray:
+    """``rng.standard_normal((n, w)) / sqrt(w)`` (spectrum.py:84, features.py:63), in place."""
+    if out is None:
+        out = np.empty((n, w), dtype=np.float64)
+    rng.standard_normal(out=out)
+    out /= np.sqrt(w)
+    return out
+
+
+def bernoulli_block(rng: np.random.Generator, n: int, w: int) -> np.ndarray:
+    """``(2 * rng.integers(0, 2, (n, w)) - 1) / sqrt(w)`` (features.py:65)."""
+    return (2.0 * rng.integers(0, 2, size=(n, w)) - 1.0) / np.sqrt(w)
+
+
+class ProbeStream:
+    """Sequential N x ds probe blocks from one generator, one block drawn ahead.
+
+    Only for generators private to the caller (run_csc's "probe" substream):
+    drawing ahead advances the generator by one extra block.
+    """
+
+    def __init__(self, rng: np.random.Generator, n: int, ds: int, pinned_buffers: bool = True):
+        self.rng, self.n, self.ds = rng, n, ds
+        mk = pinned_empty if pinned_buffers else (lambda s: np.empty(s))
+        self._bufs = [mk((n, ds)), mk((n, ds))]
+        self._i = 0
+        self._pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="csc-probe-rng")
+        self._next = self._pool.submit(normal_block, rng, n, ds, self._bufs[0])
+
+    def take(self) -> np.ndarray:
+        block = self._next.result()
+        self._i += 1
+        self._next = self._pool.submit(normal_block, self.rng, self.n, self.ds, self._bufs[self._i % 2])
+        return block
+
+    def close(self) -> None:
+        try:
+            self._next.result()
+        finally:
+            self._pool.shutdown(wait=True)

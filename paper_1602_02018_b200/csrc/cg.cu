@@ -1,0 +1,343 @@
+// K5: blocked conjugate gradient for the interpolation step (reference
+// interpolate_all, sampling.py:124-180).
+//
+// The reference runs per-column CG with shared filtering passes: each column
+// has its own alpha/beta, converged columns are frozen (alpha = beta = 0, so X
+// and R never change again).  Columns never interact, so the device runs the
+// iteration panel by panel: each panel's loop stops when its own columns have
+// converged (or at max_iters).  Per-column arithmetic, iteration counts and the
+// frozen-column semantics are unchanged; a panel whose columns are all done
+// stops costing filter passes (the reference keeps filtering them).
+//
+// Per iteration and panel: one high-pass filter whose last step fuses
+// AP = mask*P + gamma*(g(L)P + ridge*P) and the per-column P.AP partials
+// (EPI_CGAP), then alpha (fixed-order reduce), X/R update with ||R||^2
+// partials, beta + freeze bookkeeping, and P = R + beta P.
+#include <algorithm>
+#include <cmath>
+
+#include "filter.cuh"
+
+namespace csc {
+namespace {
+
+constexpr double kTiny = 2.2250738585072014e-308;  // np.finfo(np.float64).tiny, sampling.py:154
+
+int colred_grid(int device) { return device_props(device).sms * 8; }
+
+// thread -> (row slot, column) mapping shared by the column-reduction kernels:
+// column c = tid % pw, row slot = tid / pw; 256 / pw rows per block pass.
+template <typename T>
+__global__ void k_colsumsq(const T* __restrict__ A, int64_t n, int pw, int wc, double* __restrict__ part) {
+  __shared__ double red[256];
+  const int c = threadIdx.x % pw;
+  const int rs = threadIdx.x / pw;
+  const int rpb = blockDim.x / pw;
+  double s = 0.0;
+  if (c < wc && rs < rpb)
+    for (int64_t r = (int64_t)blockIdx.x * rpb + rs; r < n; r += (int64_t)gridDim.x * rpb) {
+      const double v = (double)A[r * pw + c];
+      s += v * v;
+    }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if ((int)threadIdx.x < pw) {
+    double t = 0.0;
+    for (int k = 0; k < rpb; ++k) t += red[k * pw + threadIdx.x];
+    part[(size_t)blockIdx.x * pw + threadIdx.x] = t;
+  }
+}
+
+// X += alpha P; R -= alpha AP; partial ||R||^2  (sampling.py:161-163)
+template <typename T>
+__global__ void k_cg_update(T* __restrict__ X, T* __restrict__ R, const T* __restrict__ P, const T* __restrict__ AP,
+                            const double* __restrict__ alpha, int64_t n, int pw, int wc, double* __restrict__ part) {
+  __shared__ double red[256];
+  const int c = threadIdx.x % pw;
+  const int rs = threadIdx.x / pw;
+  const int rpb = blockDim.x / pw;
+  double s = 0.0;
+  if (c < wc && rs < rpb) {
+    const double a = alpha[c];
+    for (int64_t r = (int64_t)blockIdx.x * rpb + rs; r < n; r += (int64_t)gridDim.x * rpb) {
+      const size_t o = (size_t)r * pw + c;
+      const double p = (double)P[o], ap = (double)AP[o];
+      const T x = static_cast<T>((double)X[o] + a * p);
+      const T rr = static_cast<T>((double)R[o] - a * ap);
+      X[o] = x;
+      R[o] = rr;
+      s += (double)rr * (double)rr;
+    }
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if ((int)threadIdx.x < pw) {
+    double t = 0.0;
+    for (int k = 0; k < rpb; ++k) t += red[k * pw + threadIdx.x];
+    part[(size_t)blockIdx.x * pw + threadIdx.x] = t;
+  }
+}
+
+// P = R + beta P  (sampling.py:164)
+template <typename T>
+__global__ void k_cg_direction(T* __restrict__ P, const T* __restrict__ R, const double* __restrict__ beta, int64_t n,
+                               int pw, int wc) {
+  const int64_t total = n * pw;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t % pw);
+    if (c < wc) P[t] = static_cast<T>((double)R[t] + beta[c] * (double)P[t]);
+  }
+}
+
+struct ColState {
+  double* rs;      // current ||R||^2
+  double* t2;      // (tol ||B||)^2
+  double* alpha;
+  double* beta;
+  int64_t* conv_at;
+  uint8_t* active;
+  int* nactive;    // device counter
+};
+
+// rs = ||B||^2, target^2, initial active set (sampling.py:150-153)
+__global__ void k_cg_init(const double* __restrict__ part, int64_t nblocks, int pw, int wc, double tol, ColState st) {
+  const int c = threadIdx.x;
+  if (c == 0) *st.nactive = 0;
+  __syncthreads();
+  if (c >= wc) return;
+  double s = 0.0;
+  for (int64_t b = 0; b < nblocks; ++b) s += part[b * pw + c];
+  st.rs[c] = s;
+  const double t = tol * sqrt(s);
+  st.t2[c] = t * t;
+  st.conv_at[c] = 0;
+  const bool act = s > st.t2[c];
+  st.active[c] = act ? 1 : 0;
+  if (act) atomicAdd(st.nactive, 1);
+}
+
+// alpha = rs / (P.AP) on active columns with |denom| > tiny (sampling.py:159-160)
+__global__ void k_cg_alpha(const double* __restrict__ part, int64_t nblocks, int pw, int wc, ColState st) {
+  const int c = threadIdx.x;
+  if (c >= wc) return;
+  double d = 0.0;
+  for (int64_t b = 0; b < nblocks; ++b) d += part[b * pw + c];
+  const bool ok = st.active[c] && fabs(d) > kTiny;
+  st.alpha[c] = ok ? st.rs[c] / d : 0.0;
+}
+
+// beta, rs update, freeze newly converged columns (sampling.py:164-170)
+__global__ void k_cg_beta(const double* __restrict__ part, int64_t nblocks, int pw, int wc, int64_t iter, ColState st) {
+  const int c = threadIdx.x;
+  if (c == 0) *st.nactive = 0;
+  __syncthreads();
+  if (c >= wc) return;
+  double rsn = 0.0;
+  for (int64_t b = 0; b < nblocks; ++b) rsn += part[b * pw + c];
+  const bool act = st.active[c] != 0;
+  st.beta[c] = act ? rsn / fmax(st.rs[c], kTiny) : 0.0;
+  st.rs[c] = rsn;
+  const bool done = act && rsn <= st.t2[c];
+  if (done) st.conv_at[c] = iter;
+  const bool still = act && !done;
+  st.active[c] = still ? 1 : 0;
+  if (still) atomicAdd(st.nactive, 1);
+}
+
+// residuals, converged flags, iterations of unconverged columns (sampling.py:172-175)
+__global__ void k_cg_finish(ColState st, int wc, int64_t iters, double* __restrict__ resid, uint8_t* __restrict__ conv,
+                            int64_t* __restrict__ its) {
+  const int c = threadIdx.x;
+  if (c >= wc) return;
+  const double r = sqrt(st.rs[c]);
+  resid[c] = r;
+  conv[c] = r <= sqrt(st.t2[c]) + kTiny ? 1 : 0;
+  its[c] = st.active[c] ? iters : st.conv_at[c];
+}
+
+template <typename T>
+__global__ void k_scatter_rhs(const double* __restrict__ reduced, int k, const int64_t* __restrict__ idx, int64_t n,
+                              int c0, int wc, int pw, T* __restrict__ B) {
+  const int64_t total = n * wc;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / wc;
+    const int c = (int)(t - i * wc);
+    B[(size_t)idx[i] * pw + c] = static_cast<T>(reduced[i * k + c0 + c]);
+  }
+}
+
+__global__ void k_mask(const int64_t* __restrict__ idx, int64_t n, int64_t N, uint8_t* __restrict__ mask,
+                       int* __restrict__ bad) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx[t];
+    if (i < 0 || i >= N) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    const unsigned int word = atomicOr(reinterpret_cast<unsigned int*>(mask + (i & ~3ll)), 1u << (8 * (i & 3)));
+    if (word & (1u << (8 * (i & 3)))) atomicOr(bad, 2);
+  }
+}
+
+template <typename T>
+void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double ridge, const uint8_t* mask,
+              const int64_t* idx, int64_t n, const double* reduced, int k, double tol, int64_t max_iters, int c0,
+              int pw, int wc, T* Xp, double* resid, uint8_t* conv, int64_t* its, int64_t* iters_run, cudaStream_t s) {
+  const int64_t N = g->n;
+  const size_t pb = sizeof(T) * (size_t)N * pw;
+  Scratch R(pb, s), P(pb, s), AP(pb, s), B0(pb, s), B1(pb, s), Yacc;
+  if (g_opt.recurrence.load() == 1) Yacc.alloc(pb, s);
+  const int cg = colred_grid(g->device);
+  const int cap = std::max(step_grid_cap(g->device), cg);
+  Scratch part(sizeof(double) * (size_t)cap * pw, s);
+  Scratch colmem(sizeof(double) * 4 * pw + sizeof(int64_t) * pw + pw + 64, s);
+  ColState st;
+  st.rs = colmem.as<double>();
+  st.t2 = st.rs + pw;
+  st.alpha = st.t2 + pw;
+  st.beta = st.alpha + pw;
+  st.conv_at = reinterpret_cast<int64_t*>(st.beta + pw);
+  st.active = reinterpret_cast<uint8_t*>(st.conv_at + pw);
+  st.nactive = reinterpret_cast<int*>(colmem.as<char>() + ((sizeof(double) * 4 * pw + sizeof(int64_t) * pw + pw + 15) / 16) * 16);
+
+  // X = 0; R = P = B = M^T C  (sampling.py:142-149)
+  CSC_CUDA(cudaMemsetAsync(Xp, 0, pb, s));
+  CSC_CUDA(cudaMemsetAsync(R.get(), 0, pb, s));
+  if (n > 0) {
+    const int grid = (int)std::min<int64_t>((n * wc + 255) / 256 + 1, 4096);
+    k_scatter_rhs<T><<<grid, 256, 0, s>>>(reduced, k, idx, n, c0, wc, pw, R.as<T>());
+    CSC_LAUNCHED();
+  }
+  CSC_CUDA(cudaMemcpyAsync(P.get(), R.get(), pb, cudaMemcpyDeviceToDevice, s));
+  k_colsumsq<T><<<cg, 256, 0, s>>>(R.as<T>(), N, pw, wc, part.as<double>());
+  CSC_LAUNCHED();
+  k_cg_init<<<1, 128, 0, s>>>(part.as<double>(), cg, pw, wc, tol, st);
+  CSC_LAUNCHED();
+
+  int* h_active = nullptr;
+  CSC_CUDA(cudaMallocHost(&h_active, sizeof(int)));
+  int64_t iters = 0;
+  try {
+    CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSC_CUDA(cudaStreamSynchronize(s));
+    while (*h_active > 0 && iters < max_iters) {
+      EpiExtra ex;
+      ex.part = part.as<double>();
+      ex.mask = mask;
+      ex.gamma = gamma;
+      ex.ridge = ridge;
+      ex.ap = AP.get();
+      const int fgrid = filter_panel<T>(g, hp, nc, P.as<T>(), nullptr, B0.as<T>(), B1.as<T>(), Yacc.as<T>(), pw, wc,
+                                        EPI_CGAP, ex, s);
+      k_cg_alpha<<<1, 128, 0, s>>>(part.as<double>(), fgrid, pw, wc, st);
+      CSC_LAUNCHED();
+      k_cg_update<T><<<cg, 256, 0, s>>>(Xp, R.as<T>(), P.as<T>(), AP.as<T>(), st.alpha, N, pw, wc, part.as<double>());
+      CSC_LAUNCHED();
+      ++iters;
+      k_cg_beta<<<1, 128, 0, s>>>(part.as<double>(), cg, pw, wc, iters, st);
+      CSC_LAUNCHED();
+      const int dgrid = (int)std::min<int64_t>((N * pw + 255) / 256, (int64_t)device_props(g->device).sms * 16);
+      k_cg_direction<T><<<std::max(dgrid, 1), 256, 0, s>>>(P.as<T>(), R.as<T>(), st.beta, N, pw, wc);
+      CSC_LAUNCHED();
+      CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CSC_CUDA(cudaStreamSynchronize(s));
+    }
+  } catch (...) {
+    cudaFreeHost(h_active);
+    throw;
+  }
+  cudaFreeHost(h_active);
+  k_cg_finish<<<1, 128, 0, s>>>(st, wc, iters, resid, conv, its);
+  CSC_LAUNCHED();
+  *iters_run = std::max(*iters_run, iters);
+}
+
+}  // namespace
+}  // namespace csc
+
+using namespace csc;
+
+extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int ncoeffs, double gamma, double ridge,
+                            const int64_t* sample_idx, int64_t n, const double* reduced, int k, double tol,
+                            int64_t max_iters, void* X_out, int64_t ldx, int io_dtype, int64_t* iterations,
+                            double* residuals, uint8_t* converged, int64_t* iters_run, void* stream) {
+  return guard([&] {
+    if (!g) fail(CSC_ERR_INVALID, "graph is NULL");
+    if (ncoeffs < 1 || !hp_coeffs) fail(CSC_ERR_INVALID, "need high-pass coefficients");
+    if (!(gamma > 0)) fail(CSC_ERR_INVALID, "gamma must be positive");
+    if (k < 1) fail(CSC_ERR_INVALID, "k must be >= 1");
+    if (n < 0 || n > g->n) fail(CSC_ERR_INVALID, "sample count out of range");
+    if (n > 0 && (!sample_idx || !reduced)) fail(CSC_ERR_INVALID, "sample arrays are NULL");
+    if (max_iters < 0) fail(CSC_ERR_INVALID, "max_iters must be >= 0");
+    if (io_dtype != CSC_F64 && io_dtype != CSC_F32) fail(CSC_ERR_INVALID, "io_dtype must be CSC_F64 or CSC_F32");
+    if (ldx < k) fail(CSC_ERR_INVALID, "ldx < k");
+    if (!X_out && g->n > 0) fail(CSC_ERR_INVALID, "X_out is NULL");
+    DeviceGuard dg(g->device);
+    ensure_pool(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t N = g->n;
+    const PanelPlan pp = plan_panels(N, k, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+
+    DeviceView didx(sample_idx, sizeof(int64_t) * std::max<int64_t>(n, 1), g->device, s);
+    DeviceView dred(reduced, sizeof(double) * std::max<int64_t>(n * k, 1), g->device, s);
+    Scratch mask(((size_t)N + 4) & ~size_t(3), s), bad(sizeof(int), s);
+    CSC_CUDA(cudaMemsetAsync(mask.get(), 0, mask.bytes(), s));
+    CSC_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    if (n > 0) {
+      k_mask<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(didx.as<int64_t>(), n, N,
+                                                                             mask.as<uint8_t>(), bad.as<int>());
+      CSC_LAUNCHED();
+    }
+    int hbad = 0;
+    CSC_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSC_CUDA(cudaStreamSynchronize(s));
+    if (hbad & 1) fail(CSC_ERR_INVALID, "sample index out of range");
+    if (hbad & 2) fail(CSC_ERR_INVALID, "sample indices must be distinct");
+
+    DeviceOut oit(iterations, sizeof(int64_t) * k, g->device, s);
+    DeviceOut ores(residuals, sizeof(double) * k, g->device, s);
+    DeviceOut oconv(converged, (size_t)k, g->device, s);
+    Scratch it_s, res_s, conv_s;  // sinks when the caller passes NULL
+    int64_t* d_it = oit.as<int64_t>();
+    double* d_res = ores.as<double>();
+    uint8_t* d_conv = oconv.as<uint8_t>();
+    if (!d_it) { it_s.alloc(sizeof(int64_t) * k, s); d_it = it_s.as<int64_t>(); }
+    if (!d_res) { res_s.alloc(sizeof(double) * k, s); d_res = res_s.as<double>(); }
+    if (!d_conv) { conv_s.alloc(k, s); d_conv = conv_s.as<uint8_t>(); }
+
+    Scratch xp(cs * std::max<int64_t>(pp.total, 1), s);
+    int64_t run = 0;
+    for (int j = 0; j < pp.np; ++j) {
+      if (g->dtype == CSC_F64)
+        cg_panel<double>(g, hp_coeffs, ncoeffs, gamma, ridge, mask.as<uint8_t>(), didx.as<int64_t>(), n,
+                         dred.as<double>(), k, tol, max_iters, pp.c0[j], pp.pw[j], pp.wc[j],
+                         xp.as<double>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], &run, s);
+      else
+        cg_panel<float>(g, hp_coeffs, ncoeffs, gamma, ridge, mask.as<uint8_t>(), didx.as<int64_t>(), n,
+                        dred.as<double>(), k, tol, max_iters, pp.c0[j], pp.pw[j], pp.wc[j],
+                        xp.as<float>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], &run, s);
+    }
+    if (N > 0) {
+      const bool xdev = is_device_ptr(X_out, g->device);
+      const size_t es = dtype_size(io_dtype);
+      Scratch xs;
+      void* xdst = X_out;
+      int64_t xld = ldx;
+      if (!xdev) {
+        xs.alloc(es * N * k, s);
+        xdst = xs.get();
+        xld = k;
+      }
+      unpack_panels(xp.get(), g->dtype, pp, N, xdst, io_dtype, xld, s);
+      if (!xdev)
+        CSC_CUDA(cudaMemcpy2DAsync(X_out, es * ldx, xs.get(), es * k, es * k, N, cudaMemcpyDeviceToHost, s));
+      CSC_CUDA(cudaStreamSynchronize(s));
+    }
+    oit.finish();
+    ores.finish();
+    oconv.finish();
+    CSC_CUDA(cudaStreamSynchronize(s));
+    if (iters_run) *iters_run = run;
+  });
+}

@@ -1,0 +1,1076 @@
+// K2 implementation: fused Chebyshev step kernel, panel planning, packing, and
+// the filter-level C-ABI entry points (Laplacian apply, filter, eigencount,
+// features).  See filter.cuh for the formulation.
+#include <algorithm>
+#include <chrono>
+#include <mutex>
+
+#include "filter.cuh"
+
+namespace csc {
+
+// ---------------------------------------------------------------------------
+// vector access helpers (16-byte lanes)
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int n = 4;
+  __device__ static void unpack(const float4& v, float (&a)[4]) {
+    a[0] = v.x;
+    a[1] = v.y;
+    a[2] = v.z;
+    a[3] = v.w;
+  }
+  __device__ static float4 make(const float (&a)[4]) { return make_float4(a[0], a[1], a[2], a[3]); }
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int n = 2;
+  __device__ static void unpack(const double2& v, double (&a)[2]) {
+    a[0] = v.x;
+    a[1] = v.y;
+  }
+  __device__ static double2 make(const double (&a)[2]) { return make_double2(a[0], a[1]); }
+};
+
+template <bool HINT, typename V>
+__device__ __forceinline__ V ld_stream(const V* p) {
+  if constexpr (HINT)
+    return __ldcs(p);  // evict-first: read once per step
+  else
+    return *p;
+}
+template <bool HINT, typename V>
+__device__ __forceinline__ void st_stream(V* p, const V& v) {
+  if constexpr (HINT)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+template <bool HINT, typename S>
+__device__ __forceinline__ S ld_csr(const S* p) {
+  if constexpr (HINT)
+    return __ldcs(p);
+  else
+    return __ldg(p);
+}
+
+// ---------------------------------------------------------------------------
+// The step kernel.  LPR lanes own one row of a panel (VEC elements each);
+// 32/LPR rows per warp; warps stride over row groups.  Each lane keeps U
+// neighbour gathers in flight.
+template <typename T, int LPR, int EPI, bool HINTS, int U>
+__global__ void __launch_bounds__(256) k_cheb_step(const StepArgs a) {
+  using VT = Vec16<T>;
+  using V = typename VT::type;
+  constexpr int VEC = VT::n;
+  constexpr int PW = LPR * VEC;
+  constexpr int GPW = 32 / LPR;
+
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPR;
+  const int grp = lane / LPR;
+  const int col0 = sub * VEC;
+  const bool lane_on = col0 < a.wc;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  const T* __restrict__ G = static_cast<const T*>(a.G);
+  const T* S = static_cast<const T*>(a.S);
+  const T* __restrict__ X = static_cast<const T*>(a.X);
+  const T* Yin = static_cast<const T*>(a.Yin);
+  T* O = static_cast<T*>(a.O);
+  T* Y = static_cast<T*>(a.Y);
+  const T* __restrict__ wn = static_cast<const T*>(a.wn);
+  const T ka = static_cast<T>(a.ka), ks = static_cast<T>(a.ks), kx = static_cast<T>(a.kx);
+  const T ky0 = static_cast<T>(a.ky0), ky = static_cast<T>(a.ky);
+
+  double ssq = 0.0;
+  double cd[VEC];
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) cd[c] = 0.0;
+
+  for (int64_t rb = warp * GPW; rb < a.n; rb += nwarps * GPW) {
+    const int64_t row = rb + grp;
+    const bool on = lane_on && row < a.n;
+    T acc[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) acc[c] = T(0);
+
+    if (G != nullptr && on) {
+      const int32_t beg = __ldg(a.indptr + row);
+      const int32_t end = __ldg(a.indptr + row + 1);
+      for (int32_t e = beg; e < end; e += U) {
+        int32_t j[U];
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (e + u < end) {
+            j[u] = ld_csr<HINTS>(a.indices + e + u);
+            v[u] = ld_csr<HINTS>(wn + e + u);
+          } else {
+            j[u] = -1;
+            v[u] = T(0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (j[u] >= 0) {
+            T gv[VEC];
+            VT::unpack(__ldg(reinterpret_cast<const V*>(G + (size_t)j[u] * PW + col0)), gv);
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) acc[c] = fma(v[u], gv[c], acc[c]);
+          }
+        }
+      }
+    }
+
+    double rsq = 0.0;
+    if (on) {
+      const size_t off = (size_t)row * PW + col0;
+      T out[VEC], xv[VEC], res[VEC];
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        out[c] = ka * acc[c];
+        xv[c] = T(0);
+      }
+      if (S != nullptr) {
+        T sv[VEC];
+        VT::unpack(ld_stream<HINTS>(reinterpret_cast<const V*>(S + off)), sv);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) out[c] = fma(ks, sv[c], out[c]);
+      }
+      if (X != nullptr) {
+        VT::unpack(ld_stream<HINTS>(reinterpret_cast<const V*>(X + off)), xv);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) out[c] = fma(kx, xv[c], out[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) res[c] = out[c];
+      if (a.fwd) {
+        T yv[VEC];
+        VT::unpack(ld_stream<HINTS>(reinterpret_cast<const V*>(Yin + off)), yv);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) res[c] = fma(ky, out[c], ky0 * yv[c]);
+        if (Y != nullptr) st_stream<HINTS>(reinterpret_cast<V*>(Y + off), VT::make(res));
+      }
+      if (O != nullptr) {
+        // default write-back: this panel is the next step's gather source, let it stay in L2
+        *reinterpret_cast<V*>(O + off) = VT::make(out);
+      }
+      if constexpr (EPI == EPI_SUMSQ || EPI == EPI_ROWSQ) {
+#pragma unroll
+        for (int c = 0; c < VEC; ++c)
+          if (col0 + c < a.wc) rsq += (double)res[c] * (double)res[c];
+        if constexpr (EPI == EPI_SUMSQ) ssq += rsq;
+      }
+      if constexpr (EPI == EPI_CGAP) {
+        const T m = a.mask[row] ? T(1) : T(0);
+        const double gam = a.gamma, rho = a.ridge;
+        T ap[VEC];
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          // AP = mask*P + gamma*(g(L)P + ridge*P), sampling.py:120-121
+          const double reg = (double)res[c] + rho * (double)xv[c];
+          ap[c] = static_cast<T>((double)(m * xv[c]) + gam * reg);
+          if (col0 + c < a.wc) cd[c] += (double)xv[c] * (double)ap[c];
+        }
+        st_stream<HINTS>(reinterpret_cast<V*>(static_cast<T*>(a.E) + off), VT::make(ap));
+      }
+    }
+    if constexpr (EPI == EPI_ROWSQ) {
+#pragma unroll
+      for (int o = LPR / 2; o >= 1; o >>= 1) rsq += __shfl_xor_sync(0xffffffffu, rsq, o);
+      if (sub == 0 && row < a.n) a.part[row] = rsq;
+    }
+  }
+
+  // block-level epilogue reductions (fixed order -> deterministic)
+  if constexpr (EPI == EPI_SUMSQ) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+    if (lane == 0) red[threadIdx.x >> 5] = ssq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      a.part[blockIdx.x] = t;
+    }
+  }
+  if constexpr (EPI == EPI_CGAP) {
+    __shared__ double red[8][PW];  // <= 256 threads (launch bounds)
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) {
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) cd[c] += __shfl_xor_sync(0xffffffffu, cd[c], o);
+    }
+    if (grp == 0) {
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) red[threadIdx.x >> 5][col0 + c] = cd[c];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < PW; t += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][t];
+      a.part[(size_t)blockIdx.x * PW + t] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+template <typename T, int LPR, int EPI, bool HINTS, int U>
+static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t s) {
+  auto kern = k_cheb_step<T, LPR, EPI, HINTS, U>;
+  static std::mutex mu;
+  static int occ_cache[64] = {0};  // per device
+  int occ;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const int slot = (device & 7) * 8 + ((threads / 32 - 1) & 7);
+    if (occ_cache[slot] == 0) {
+      int o = 0;
+      CSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, 0));
+      occ_cache[slot] = std::max(o, 1);
+    }
+    occ = occ_cache[slot];
+  }
+  const int64_t rows_per_block = (int64_t)(threads / 32) * (32 / LPR);
+  int64_t need = (a.n + rows_per_block - 1) / rows_per_block;
+  const int64_t cap = std::min<int64_t>((int64_t)device_props(device).sms * occ, step_grid_cap(device));
+  const int grid = (int)std::max<int64_t>(1, std::min(need, cap));
+  kern<<<grid, threads, 0, s>>>(a);
+  CSC_LAUNCHED();
+  return grid;
+}
+
+template <typename T, int EPI, bool HINTS, int U>
+static int launch_lpr(const StepArgs& a, int lpr, int threads, int device, cudaStream_t s) {
+  switch (lpr) {
+    case 1: return launch_typed<T, 1, EPI, HINTS, U>(a, threads, device, s);
+    case 2: return launch_typed<T, 2, EPI, HINTS, U>(a, threads, device, s);
+    case 4: return launch_typed<T, 4, EPI, HINTS, U>(a, threads, device, s);
+    case 8: return launch_typed<T, 8, EPI, HINTS, U>(a, threads, device, s);
+    case 16: return launch_typed<T, 16, EPI, HINTS, U>(a, threads, device, s);
+    case 32: return launch_typed<T, 32, EPI, HINTS, U>(a, threads, device, s);
+  }
+  fail(CSC_ERR_INVALID, "unsupported panel width");
+}
+
+template <typename T, int EPI>
+static int launch_epi(const StepArgs& a, int lpr, int threads, int device, cudaStream_t s) {
+  const bool hints = g_opt.cache_hints.load() != 0;
+  const int unroll = (int)g_opt.unroll.load();
+  if (hints) {
+    if (unroll == 4) return launch_lpr<T, EPI, true, 4>(a, lpr, threads, device, s);
+    return launch_lpr<T, EPI, true, 8>(a, lpr, threads, device, s);
+  }
+  if (unroll == 4) return launch_lpr<T, EPI, false, 4>(a, lpr, threads, device, s);
+  return launch_lpr<T, EPI, false, 8>(a, lpr, threads, device, s);
+}
+
+int step_grid_cap(int device) {
+  // 2048 resident threads per SM at most; block_threads >= 64
+  return device_props(device).sms * 32;
+}
+
+static double step_bytes(const csc_graph* g, const StepArgs& a, int epi) {
+  const double s = (double)dtype_size(g->dtype);
+  const double nw = (double)a.n * a.wc * s;
+  double b = 0.0;
+  if (a.G) b += 4.0 * (g->n + 1) + (double)g->nnz * (4.0 + s) + nw;  // CSR + one compulsory read of G
+  if (a.S) b += nw;
+  if (a.X) b += nw;
+  if (a.O) b += nw;
+  if (a.fwd) b += nw + (a.Y ? nw : 0.0);
+  if (epi == EPI_CGAP) b += nw + (double)a.n;  // AP write + mask
+  if (epi == EPI_ROWSQ) b += 8.0 * a.n;
+  return b;
+}
+
+template <typename T>
+int launch_step(const csc_graph* g, const StepArgs& a, int pw, int epi, cudaStream_t s) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int lpr = pw / VEC;
+  const int threads = (int)g_opt.block_threads.load();
+  const bool prof = g_opt.profile.load() != 0 && a.G != nullptr;
+  cudaEvent_t e0 = nullptr;
+  if (prof) profile_begin(s, &e0);
+  int grid = 0;
+  switch (epi) {
+    case EPI_NONE: grid = launch_epi<T, EPI_NONE>(a, lpr, threads, g->device, s); break;
+    case EPI_SUMSQ: grid = launch_epi<T, EPI_SUMSQ>(a, lpr, threads, g->device, s); break;
+    case EPI_ROWSQ: grid = launch_epi<T, EPI_ROWSQ>(a, lpr, threads, g->device, s); break;
+    case EPI_CGAP: grid = launch_epi<T, EPI_CGAP>(a, lpr, threads, g->device, s); break;
+    default: fail(CSC_ERR_INVALID, "bad epilogue");
+  }
+  if (prof) profile_end(s, e0, step_bytes(g, a, epi));
+  return grid;
+}
+
+template int launch_step<float>(const csc_graph*, const StepArgs&, int, int, cudaStream_t);
+template int launch_step<double>(const csc_graph*, const StepArgs&, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// filter drivers
+template <typename T>
+int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, T* B0, T* B1, T* Yacc, int pw,
+                 int wc, int epi, const EpiExtra& ex, cudaStream_t s) {
+  const int p = nc - 1;
+  auto base = [&]() {
+    StepArgs a{};
+    a.indptr = g->indptr;
+    a.indices = g->indices;
+    a.wn = g->wn;
+    a.n = g->n;
+    a.wc = wc;
+    return a;
+  };
+  auto with_epi = [&](StepArgs a, int e) {
+    a.part = ex.part;
+    if (e == EPI_CGAP) {
+      a.mask = ex.mask;
+      a.gamma = ex.gamma;
+      a.ridge = ex.ridge;
+      a.E = ex.ap;
+    }
+    return a;
+  };
+  auto run = [&](StepArgs a, int e) { return launch_step<T>(g, with_epi(a, e), pw, e, s); };
+
+  if (p == 0) {  // Y = c_0 X  (order 0: filters.py:147 leaves out = c[0] * x)
+    StepArgs a = base();
+    a.X = X;
+    a.kx = c[0];
+    a.O = Y;
+    return run(a, epi);
+  }
+  const bool forward = g_opt.recurrence.load() == 1;
+  if (!forward) {
+    // Clenshaw: b_l = c_l X + 2A b_{l+1} - b_{l+2}, A = L - I = -Wn; Y = c_0 X + A b_1 - b_2
+    if (p == 1) {
+      StepArgs a = base();
+      a.G = X;
+      a.ka = -c[1];
+      a.X = X;
+      a.kx = c[0];
+      a.O = Y;
+      return run(a, epi);
+    }
+    StepArgs a = base();
+    a.G = X;  // b_{p-1} = c_{p-1} X + 2 c_p A X
+    a.ka = -2.0 * c[p];
+    a.X = X;
+    a.kx = c[p - 1];
+    a.O = B0;
+    run(a, EPI_NONE);
+    if (p == 2) {  // Y = c_0 X + A b_1 - b_2, b_2 = c_2 X
+      StepArgs f = base();
+      f.G = B0;
+      f.ka = -1.0;
+      f.X = X;
+      f.kx = c[0] - c[2];
+      f.O = Y;
+      return run(f, epi);
+    }
+    StepArgs b = base();  // b_{p-2} = c_{p-2} X + 2A b_{p-1} - c_p X
+    b.G = B0;
+    b.ka = -2.0;
+    b.X = X;
+    b.kx = c[p - 2] - c[p];
+    b.O = B1;
+    run(b, EPI_NONE);
+    T* cur = B1;  // b_{l+1}
+    T* prv = B0;  // b_{l+2}
+    for (int l = p - 3; l >= 1; --l) {
+      StepArgs m = base();
+      m.G = cur;
+      m.ka = -2.0;
+      m.S = prv;
+      m.ks = -1.0;
+      m.X = X;
+      m.kx = c[l];
+      m.O = prv;  // b_l overwrites b_{l+2} row by row
+      run(m, EPI_NONE);
+      std::swap(cur, prv);
+    }
+    StepArgs f = base();
+    f.G = cur;
+    f.ka = -1.0;
+    f.S = prv;
+    f.ks = -1.0;
+    f.X = X;
+    f.kx = c[0];
+    f.O = Y;
+    return run(f, epi);
+  }
+
+  // forward recurrence (filters.py:148-154)
+  T* acc = Y ? Y : Yacc;
+  if (!acc) fail(CSC_ERR_INVALID, "forward recurrence needs an accumulator panel");
+  const T* xe = (epi == EPI_CGAP) ? X : nullptr;  // CGAP reads P on the final step
+  {
+    StepArgs a = base();  // T_1 = (L - I) X;  Y = c_0 X + c_1 T_1
+    a.G = X;
+    a.ka = -1.0;
+    a.O = (p == 1) ? nullptr : B0;
+    a.fwd = 1;
+    a.Yin = X;
+    a.ky0 = c[0];
+    a.ky = c[1];
+    a.Y = (p == 1) ? Y : acc;
+    if (p == 1) {
+      a.X = xe;
+      return run(a, epi);
+    }
+    run(a, EPI_NONE);
+  }
+  const T* t_prev = X;  // T_{l-2}
+  T* t_cur = B0;        // T_{l-1}
+  T* spare = B1;
+  for (int l = 2; l <= p; ++l) {
+    const bool last = l == p;
+    StepArgs a = base();
+    a.G = t_cur;
+    a.ka = -2.0;
+    a.S = t_prev;
+    a.ks = -1.0;
+    T* dst = (t_prev == X) ? spare : const_cast<T*>(t_prev);
+    a.O = last ? nullptr : dst;
+    a.fwd = 1;
+    a.Yin = acc;
+    a.ky0 = 1.0;
+    a.ky = c[l];
+    a.Y = last ? Y : acc;
+    if (last) {
+      a.X = xe;
+      return run(a, epi);
+    }
+    run(a, EPI_NONE);
+    t_prev = t_cur;
+    t_cur = dst;
+  }
+  return 0;  // unreachable
+}
+
+template int filter_panel<float>(const csc_graph*, const double*, int, const float*, float*, float*, float*, float*,
+                                 int, int, int, const EpiExtra&, cudaStream_t);
+template int filter_panel<double>(const csc_graph*, const double*, int, const double*, double*, double*, double*,
+                                  double*, int, int, int, const EpiExtra&, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// panels
+PanelPlan plan_panels(int64_t n, int w, int dtype, int device) {
+  const int vec = 16 / (int)dtype_size(dtype);
+  const int max_lpr = 32;
+  int max_pw = vec * max_lpr;
+  const int64_t forced = g_opt.panel_width.load();
+  if (forced > 0) {
+    int pw = vec;
+    while (pw < forced && pw < max_pw) pw *= 2;
+    max_pw = pw;
+  } else {
+    // widest power-of-two panel whose gather source fits the L2 budget
+    const double budget = (double)device_props(device).l2_bytes * (double)g_opt.l2_budget_pct.load() / 100.0;
+    int pw = vec;
+    while (pw * 2 <= max_pw && (double)n * (pw * 2) * dtype_size(dtype) <= budget) pw *= 2;
+    if ((double)n * pw * dtype_size(dtype) > budget) pw = max_pw;  // nothing fits: minimise CSR passes
+    max_pw = pw;
+  }
+  PanelPlan pp;
+  int c0 = 0;
+  int64_t off = 0;
+  while (c0 < w) {
+    const int rem = w - c0;
+    int pw;
+    if (rem >= max_pw) {
+      pw = max_pw;
+    } else {
+      pw = vec;
+      while (pw < rem) pw *= 2;
+    }
+    const int wc = std::min(pw, rem);
+    pp.pw.push_back(pw);
+    pp.wc.push_back(wc);
+    pp.c0.push_back(c0);
+    pp.off.push_back(off);
+    off += (int64_t)n * pw;
+    pp.max_pw = std::max(pp.max_pw, pw);
+    c0 += wc;
+  }
+  pp.np = (int)pp.pw.size();
+  pp.total = off;
+  return pp;
+}
+
+template <typename Ti, typename To>
+__global__ void k_pack(const Ti* __restrict__ src, int64_t ld, int c0, int wc, int pw, int64_t n, To* __restrict__ dst) {
+  const int64_t total = n * pw;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / pw;
+    const int c = (int)(t - row * pw);
+    dst[t] = c < wc ? static_cast<To>(src[row * ld + c0 + c]) : To(0);
+  }
+}
+
+template <typename Ti, typename To>
+__global__ void k_unpack(const Ti* __restrict__ src, int c0, int wc, int pw, int64_t n, To* __restrict__ dst, int64_t ld) {
+  const int64_t total = n * wc;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / wc;
+    const int c = (int)(t - row * wc);
+    dst[row * ld + c0 + c] = static_cast<To>(src[row * pw + c]);
+  }
+}
+
+static int ew_grid(int64_t work) {
+  int64_t g = (work + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64));
+}
+
+void pack_panels(const void* src, int io_dtype, int64_t ld, void* dst, int dtype, const PanelPlan& pp, int64_t n,
+                 cudaStream_t s) {
+  for (int j = 0; j < pp.np; ++j) {
+    const int64_t work = n * pp.pw[j];
+    if (work == 0) continue;
+    const int gsz = ew_grid(work);
+    if (io_dtype == CSC_F64 && dtype == CSC_F64)
+      k_pack<double, double><<<gsz, 256, 0, s>>>((const double*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                                 (double*)dst + pp.off[j]);
+    else if (io_dtype == CSC_F64 && dtype == CSC_F32)
+      k_pack<double, float><<<gsz, 256, 0, s>>>((const double*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                                (float*)dst + pp.off[j]);
+    else if (io_dtype == CSC_F32 && dtype == CSC_F64)
+      k_pack<float, double><<<gsz, 256, 0, s>>>((const float*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                                (double*)dst + pp.off[j]);
+    else
+      k_pack<float, float><<<gsz, 256, 0, s>>>((const float*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                               (float*)dst + pp.off[j]);
+    CSC_LAUNCHED();
+  }
+}
+
+void unpack_panels(const void* src, int dtype, const PanelPlan& pp, int64_t n, void* dst, int io_dtype, int64_t ld,
+                   cudaStream_t s) {
+  for (int j = 0; j < pp.np; ++j) {
+    const int64_t work = n * pp.wc[j];
+    if (work == 0) continue;
+    const int gsz = ew_grid(work);
+    if (dtype == CSC_F64 && io_dtype == CSC_F64)
+      k_unpack<double, double><<<gsz, 256, 0, s>>>((const double*)src + pp.off[j], pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                                   (double*)dst, ld);
+    else if (dtype == CSC_F32 && io_dtype == CSC_F64)
+      k_unpack<float, double><<<gsz, 256, 0, s>>>((const float*)src + pp.off[j], pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                                  (double*)dst, ld);
+    else if (dtype == CSC_F64 && io_dtype == CSC_F32)
+      k_unpack<double, float><<<gsz, 256, 0, s>>>((const double*)src + pp.off[j], pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                                  (float*)dst, ld);
+    else
+      k_unpack<float, float><<<gsz, 256, 0, s>>>((const float*)src + pp.off[j], pp.c0[j], pp.wc[j], pp.pw[j], n,
+                                                 (float*)dst, ld);
+    CSC_LAUNCHED();
+  }
+}
+
+// fixed-order reductions
+__global__ void k_reduce_sum(const double* __restrict__ in, int64_t count, double* __restrict__ out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += in[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o >= 1; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+__global__ void k_reduce_cols(const double* __restrict__ in, int64_t nblocks, int stride, int ncols,
+                              double* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) s += in[b * stride + c];
+    out[c] = s;
+  }
+}
+
+void reduce_sum(const double* in, int64_t count, double* out, cudaStream_t s) {
+  k_reduce_sum<<<1, 256, 0, s>>>(in, count, out);
+  CSC_LAUNCHED();
+}
+
+void reduce_cols(const double* in, int64_t nblocks, int stride, int ncols, double* out, cudaStream_t s) {
+  k_reduce_cols<<<(ncols + 127) / 128, 128, 0, s>>>(in, nblocks, stride, ncols, out);
+  CSC_LAUNCHED();
+}
+
+// features: sum panel row-norms in panel order, normalise, flag zero rows
+template <typename T, typename To>
+__global__ void k_normalize_rows(const T* __restrict__ Yp, const double* __restrict__ rowsq, int np,
+                                 const int* __restrict__ pw, const int* __restrict__ wc, const int* __restrict__ c0,
+                                 const int64_t* __restrict__ off, int64_t n, To* __restrict__ F, int64_t ldf,
+                                 uint8_t* __restrict__ zflag, unsigned long long* __restrict__ nzero) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = warp; row < n; row += nw) {
+    double t = 0.0;
+    for (int j = 0; j < np; ++j) t += rowsq[(int64_t)j * n + row];
+    const double nrm = sqrt(t);
+    const bool zero = nrm <= 1e-300;  // features.py:23, 81
+    for (int j = 0; j < np; ++j) {
+      const T* src = Yp + off[j] + row * pw[j];
+      for (int c = lane; c < wc[j]; c += 32) {
+        const double v = (double)src[c];
+        F[row * ldf + c0[j] + c] = zero ? To(0) : static_cast<To>(v / nrm);
+      }
+    }
+    if (lane == 0) {
+      if (zflag) zflag[row] = zero ? 1 : 0;
+      if (zero) atomicAdd(nzero, 1ull);
+    }
+  }
+}
+
+__global__ void k_sum_panels(const double* __restrict__ rowsq, int np, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int j = 0; j < np; ++j) t += rowsq[(int64_t)j * n + i];
+    out[i] = t;
+  }
+}
+
+template <typename T>
+__global__ void k_normalize_rowmajor(const T* __restrict__ Y, int64_t ldy, int64_t n, int w,
+                                     const double* __restrict__ rowsq, T* __restrict__ F, int64_t ldf,
+                                     uint8_t* __restrict__ zflag, unsigned long long* __restrict__ nzero) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = warp; row < n; row += nw) {
+    const double nrm = sqrt(rowsq[row]);
+    const bool zero = nrm <= 1e-300;
+    for (int c = lane; c < w; c += 32) {
+      const double v = (double)Y[row * ldy + c];
+      F[row * ldf + c] = zero ? T(0) : static_cast<T>(v / nrm);
+    }
+    if (lane == 0) {
+      if (zflag) zflag[row] = zero ? 1 : 0;
+      if (zero) atomicAdd(nzero, 1ull);
+    }
+  }
+}
+
+}  // namespace csc
+
+using namespace csc;
+
+// ---------------------------------------------------------------------------
+// C ABI (filter level)
+namespace {
+
+struct BlockIO {
+  int64_t n;
+  int w;
+  int io;
+};
+
+void check_graph(const csc_graph* g) {
+  if (!g) fail(CSC_ERR_INVALID, "graph is NULL");
+}
+
+void check_block(const csc_graph* g, const void* p, int64_t ld, int ncols, int io, const char* what) {
+  if (ncols < 0) fail(CSC_ERR_INVALID, std::string(what) + ": ncols must be >= 0");
+  if (io != CSC_F64 && io != CSC_F32) fail(CSC_ERR_INVALID, "io_dtype must be CSC_F64 or CSC_F32");
+  if (ld < ncols) fail(CSC_ERR_INVALID, std::string(what) + ": leading dimension smaller than ncols");
+  if (p == nullptr && g->n > 0 && ncols > 0) fail(CSC_ERR_INVALID, std::string(what) + " is NULL");
+}
+
+void check_coeffs(const double* c, int nc) {
+  if (nc < 1) fail(CSC_ERR_INVALID, "need at least one coefficient");
+  if (!c) fail(CSC_ERR_INVALID, "coefficients are NULL");
+}
+
+// Stage a row-major (n x ncols, ld) input on the device; returns pointer + ld.
+struct StagedIn {
+  const void* p = nullptr;
+  int64_t ld = 0;
+  Scratch buf;
+};
+void stage_in(const void* src, int64_t ld, int64_t n, int ncols, int io, int device, cudaStream_t s, StagedIn& out) {
+  const size_t es = dtype_size(io);
+  if (is_device_ptr(src, device)) {
+    out.p = src;
+    out.ld = ld;
+    return;
+  }
+  out.buf.alloc(es * n * ncols, s);
+  CSC_CUDA(cudaMemcpy2DAsync(out.buf.get(), es * ncols, src, es * ld, es * ncols, n, cudaMemcpyHostToDevice, s));
+  out.p = out.buf.get();
+  out.ld = ncols;
+}
+
+struct StagedOut {
+  void* p = nullptr;  // device target
+  int64_t ld = 0;
+  void* host = nullptr;
+  int64_t host_ld = 0;
+  Scratch buf;
+};
+void stage_out(void* dst, int64_t ld, int64_t n, int ncols, int io, int device, cudaStream_t s, StagedOut& out) {
+  const size_t es = dtype_size(io);
+  if (is_device_ptr(dst, device)) {
+    out.p = dst;
+    out.ld = ld;
+    return;
+  }
+  out.buf.alloc(es * n * ncols, s);
+  out.p = out.buf.get();
+  out.ld = ncols;
+  out.host = dst;
+  out.host_ld = ld;
+}
+void finish_out(StagedOut& o, int64_t n, int ncols, int io, cudaStream_t s) {
+  if (!o.host) return;
+  const size_t es = dtype_size(io);
+  CSC_CUDA(cudaMemcpy2DAsync(o.host, es * o.host_ld, o.p, es * ncols, es * ncols, n, cudaMemcpyDeviceToHost, s));
+}
+
+template <typename T>
+void run_filter_all(const csc_graph* g, const double* coeffs, int nc, const PanelPlan& pp, const T* Xp, T* Yp,
+                    int epi, double* part, int64_t part_stride, cudaStream_t s) {
+  Scratch b0(sizeof(T) * g->n * pp.max_pw, s), b1(sizeof(T) * g->n * pp.max_pw, s);
+  Scratch yacc;
+  if (!Yp && g_opt.recurrence.load() == 1) yacc.alloc(sizeof(T) * g->n * pp.max_pw, s);
+  for (int j = 0; j < pp.np; ++j) {
+    EpiExtra ex;
+    ex.part = part ? part + part_stride * j : nullptr;
+    filter_panel<T>(g, coeffs, nc, Xp + pp.off[j], Yp ? Yp + pp.off[j] : nullptr, b0.as<T>(), b1.as<T>(),
+                    yacc.as<T>(), pp.pw[j], pp.wc[j], epi, ex, s);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int csc_laplacian_apply(const csc_graph* g, const void* X, int64_t ldx, void* Y, int64_t ldy, int ncols, int io_dtype,
+                        void* stream) {
+  return guard([&] {
+    check_graph(g);
+    check_block(g, X, ldx, ncols, io_dtype, "X");
+    check_block(g, Y, ldy, ncols, io_dtype, "Y");
+    if (g->n == 0 || ncols == 0) return;
+    DeviceGuard dg(g->device);
+    ensure_pool(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+    StagedIn xin;
+    stage_in(X, ldx, g->n, ncols, io_dtype, g->device, s, xin);
+    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s);
+    pack_panels(xin.p, io_dtype, xin.ld, xp.get(), g->dtype, pp, g->n, s);
+    for (int j = 0; j < pp.np; ++j) {  // L X = X - Wn X  (graph.py:154-155)
+      StepArgs a{};
+      a.indptr = g->indptr;
+      a.indices = g->indices;
+      a.wn = g->wn;
+      a.n = g->n;
+      a.wc = pp.wc[j];
+      a.ka = -1.0;
+      a.kx = 1.0;
+      if (g->dtype == CSC_F64) {
+        a.G = xp.as<double>() + pp.off[j];
+        a.X = a.G;
+        a.O = yp.as<double>() + pp.off[j];
+        launch_step<double>(g, a, pp.pw[j], EPI_NONE, s);
+      } else {
+        a.G = xp.as<float>() + pp.off[j];
+        a.X = a.G;
+        a.O = yp.as<float>() + pp.off[j];
+        launch_step<float>(g, a, pp.pw[j], EPI_NONE, s);
+      }
+    }
+    StagedOut yo;
+    stage_out(Y, ldy, g->n, ncols, io_dtype, g->device, s, yo);
+    unpack_panels(yp.get(), g->dtype, pp, g->n, yo.p, io_dtype, yo.ld, s);
+    finish_out(yo, g->n, ncols, io_dtype, s);
+    if (yo.host) CSC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int csc_cheb_filter(const csc_graph* g, const double* coeffs, int ncoeffs, const void* X, int64_t ldx, void* Y,
+                    int64_t ldy, int ncols, int io_dtype, void* stream) {
+  return guard([&] {
+    check_graph(g);
+    check_coeffs(coeffs, ncoeffs);
+    check_block(g, X, ldx, ncols, io_dtype, "X");
+    check_block(g, Y, ldy, ncols, io_dtype, "Y");
+    if (g->n == 0 || ncols == 0) return;
+    DeviceGuard dg(g->device);
+    ensure_pool(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+    StagedIn xin;
+    stage_in(X, ldx, g->n, ncols, io_dtype, g->device, s, xin);
+    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s);
+    pack_panels(xin.p, io_dtype, xin.ld, xp.get(), g->dtype, pp, g->n, s);
+    if (g->dtype == CSC_F64)
+      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), yp.as<double>(), EPI_NONE, nullptr, 0, s);
+    else
+      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), yp.as<float>(), EPI_NONE, nullptr, 0, s);
+    StagedOut yo;
+    stage_out(Y, ldy, g->n, ncols, io_dtype, g->device, s, yo);
+    unpack_panels(yp.get(), g->dtype, pp, g->n, yo.p, io_dtype, yo.ld, s);
+    finish_out(yo, g->n, ncols, io_dtype, s);
+    if (yo.host) CSC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int csc_eigencount(const csc_graph* g, const double* coeffs, int ncoeffs, const void* R, int64_t ldr, int ncols,
+                   int io_dtype, double* count, void* stream) {
+  return guard([&] {
+    check_graph(g);
+    check_coeffs(coeffs, ncoeffs);
+    check_block(g, R, ldr, ncols, io_dtype, "R");
+    if (!count) fail(CSC_ERR_INVALID, "count is NULL");
+    DeviceGuard dg(g->device);
+    ensure_pool(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (g->n == 0 || ncols == 0) {
+      DeviceOut co(count, sizeof(double), g->device, s);
+      CSC_CUDA(cudaMemsetAsync(co.as<double>(), 0, sizeof(double), s));
+      co.finish();
+      CSC_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+    StagedIn rin;
+    stage_in(R, ldr, g->n, ncols, io_dtype, g->device, s, rin);
+    Scratch xp(cs * pp.total, s);
+    pack_panels(rin.p, io_dtype, rin.ld, xp.get(), g->dtype, pp, g->n, s);
+    const int cap = step_grid_cap(g->device);
+    Scratch part(sizeof(double) * (size_t)cap * pp.np, s);
+    CSC_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * (size_t)cap * pp.np, s));
+    if (g->dtype == CSC_F64)
+      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), nullptr, EPI_SUMSQ, part.as<double>(), cap, s);
+    else
+      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), nullptr, EPI_SUMSQ, part.as<double>(), cap, s);
+    DeviceOut co(count, sizeof(double), g->device, s);
+    reduce_sum(part.as<double>(), (int64_t)cap * pp.np, co.as<double>(), s);
+    co.finish();
+    if (co.on_host()) CSC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int csc_filter_rowsq(const csc_graph* g, const double* coeffs, int ncoeffs, const void* R, int64_t ldr, int ncols,
+                     int io_dtype, void* Y, int64_t ldy, double* rowsq, void* stream) {
+  return guard([&] {
+    check_graph(g);
+    check_coeffs(coeffs, ncoeffs);
+    check_block(g, R, ldr, ncols, io_dtype, "R");
+    check_block(g, Y, ldy, ncols, io_dtype, "Y");
+    if (!rowsq && g->n > 0) fail(CSC_ERR_INVALID, "rowsq is NULL");
+    DeviceGuard dg(g->device);
+    ensure_pool(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t n = g->n;
+    if (n == 0) return;
+    DeviceOut ro(rowsq, sizeof(double) * n, g->device, s);
+    if (ncols == 0) {
+      CSC_CUDA(cudaMemsetAsync(ro.as<double>(), 0, sizeof(double) * n, s));
+      ro.finish();
+      CSC_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    const PanelPlan pp = plan_panels(n, ncols, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+    StagedIn rin;
+    stage_in(R, ldr, n, ncols, io_dtype, g->device, s, rin);
+    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s), part(sizeof(double) * n * pp.np, s);
+    pack_panels(rin.p, io_dtype, rin.ld, xp.get(), g->dtype, pp, n, s);
+    if (g->dtype == CSC_F64)
+      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), yp.as<double>(), EPI_ROWSQ, part.as<double>(), n, s);
+    else
+      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), yp.as<float>(), EPI_ROWSQ, part.as<double>(), n, s);
+    k_sum_panels<<<ew_grid(n), 256, 0, s>>>(part.as<double>(), pp.np, n, ro.as<double>());
+    CSC_LAUNCHED();
+    StagedOut yo;
+    stage_out(Y, ldy, n, ncols, io_dtype, g->device, s, yo);
+    unpack_panels(yp.get(), g->dtype, pp, n, yo.p, io_dtype, yo.ld, s);
+    finish_out(yo, n, ncols, io_dtype, s);
+    ro.finish();
+    CSC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int csc_normalize_rows(const void* Y, int64_t ldy, int64_t num_rows, int ncols, int io_dtype, const double* rowsq,
+                       void* F, int64_t ldf, uint8_t* zero_flags, int64_t* num_zero, int device, void* stream) {
+  return guard([&] {
+    if (num_rows < 0 || ncols < 0 || ldy < ncols || ldf < ncols) fail(CSC_ERR_INVALID, "bad block shape");
+    const size_t es = dtype_size(io_dtype);
+    if (num_rows == 0) {
+      if (num_zero) *num_zero = 0;
+      return;
+    }
+    if (!Y || !F || !rowsq) fail(CSC_ERR_INVALID, "NULL buffer");
+    DeviceGuard dg(device);
+    ensure_pool(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    StagedIn yin;
+    stage_in(Y, ldy, num_rows, ncols, io_dtype, device, s, yin);
+    DeviceView rq(rowsq, sizeof(double) * num_rows, device, s);
+    StagedOut fo;
+    stage_out(F, ldf, num_rows, ncols, io_dtype, device, s, fo);
+    DeviceOut zo(zero_flags, (size_t)num_rows, device, s);
+    Scratch nz(sizeof(unsigned long long), s);
+    CSC_CUDA(cudaMemsetAsync(nz.get(), 0, sizeof(unsigned long long), s));
+    const int grid = (int)std::min<int64_t>((num_rows + 7) / 8, (int64_t)device_props(device).sms * 16);
+    if (io_dtype == CSC_F64)
+      k_normalize_rowmajor<double><<<grid, 256, 0, s>>>((const double*)yin.p, yin.ld, num_rows, ncols,
+                                                        rq.as<double>(), (double*)fo.p, fo.ld, zo.as<uint8_t>(),
+                                                        nz.as<unsigned long long>());
+    else
+      k_normalize_rowmajor<float><<<grid, 256, 0, s>>>((const float*)yin.p, yin.ld, num_rows, ncols,
+                                                       rq.as<double>(), (float*)fo.p, fo.ld, zo.as<uint8_t>(),
+                                                       nz.as<unsigned long long>());
+    CSC_LAUNCHED();
+    (void)es;
+    finish_out(fo, num_rows, ncols, io_dtype, s);
+    zo.finish();
+    unsigned long long hz = 0;
+    CSC_CUDA(cudaMemcpyAsync(&hz, nz.get(), sizeof(hz), cudaMemcpyDeviceToHost, s));
+    CSC_CUDA(cudaStreamSynchronize(s));
+    if (num_zero) *num_zero = (int64_t)hz;
+  });
+}
+
+int csc_system_apply(const csc_graph* g, const double* hp_coeffs, int ncoeffs, double gamma, double ridge,
+                     const uint8_t* mask, const void* X, int64_t ldx, void* AP, int64_t ldap, int ncols, int io_dtype,
+                     void* stream) {
+  return guard([&] {
+    check_graph(g);
+    check_coeffs(hp_coeffs, ncoeffs);
+    check_block(g, X, ldx, ncols, io_dtype, "X");
+    check_block(g, AP, ldap, ncols, io_dtype, "AP");
+    if (g->n == 0 || ncols == 0) return;
+    if (!mask) fail(CSC_ERR_INVALID, "mask is NULL");
+    DeviceGuard dg(g->device);
+    ensure_pool(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+    StagedIn xin;
+    stage_in(X, ldx, g->n, ncols, io_dtype, g->device, s, xin);
+    DeviceView dm(mask, (size_t)g->n, g->device, s);
+    Scratch xp(cs * pp.total, s), ap(cs * pp.total, s);
+    pack_panels(xin.p, io_dtype, xin.ld, xp.get(), g->dtype, pp, g->n, s);
+    const int cap = step_grid_cap(g->device);
+    Scratch part(sizeof(double) * (size_t)cap * pp.max_pw, s);
+    Scratch b0(cs * g->n * pp.max_pw, s), b1(cs * g->n * pp.max_pw, s), yacc;
+    if (g_opt.recurrence.load() == 1) yacc.alloc(cs * g->n * pp.max_pw, s);
+    for (int j = 0; j < pp.np; ++j) {
+      EpiExtra ex;
+      ex.part = part.as<double>();
+      ex.mask = dm.as<uint8_t>();
+      ex.gamma = gamma;
+      ex.ridge = ridge;
+      if (g->dtype == CSC_F64) {
+        ex.ap = ap.as<double>() + pp.off[j];
+        filter_panel<double>(g, hp_coeffs, ncoeffs, xp.as<double>() + pp.off[j], nullptr, b0.as<double>(),
+                             b1.as<double>(), yacc.as<double>(), pp.pw[j], pp.wc[j], EPI_CGAP, ex, s);
+      } else {
+        ex.ap = ap.as<float>() + pp.off[j];
+        filter_panel<float>(g, hp_coeffs, ncoeffs, xp.as<float>() + pp.off[j], nullptr, b0.as<float>(),
+                            b1.as<float>(), yacc.as<float>(), pp.pw[j], pp.wc[j], EPI_CGAP, ex, s);
+      }
+    }
+    StagedOut ao;
+    stage_out(AP, ldap, g->n, ncols, io_dtype, g->device, s, ao);
+    unpack_panels(ap.get(), g->dtype, pp, g->n, ao.p, io_dtype, ao.ld, s);
+    finish_out(ao, g->n, ncols, io_dtype, s);
+    CSC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, const void* R, int64_t ldr, int ncols,
+                       int io_dtype, void* F, int64_t ldf, uint8_t* zero_flags, int64_t* num_zero, void* stream) {
+  return guard([&] {
+    check_graph(g);
+    check_coeffs(coeffs, ncoeffs);
+    check_block(g, R, ldr, ncols, io_dtype, "R");
+    check_block(g, F, ldf, ncols, io_dtype, "F");
+    DeviceGuard dg(g->device);
+    ensure_pool(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (g->n == 0 || ncols == 0) {
+      if (num_zero) *num_zero = 0;
+      return;
+    }
+    const int64_t n = g->n;
+    const PanelPlan pp = plan_panels(n, ncols, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+    StagedIn rin;
+    stage_in(R, ldr, n, ncols, io_dtype, g->device, s, rin);
+    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s);
+    pack_panels(rin.p, io_dtype, rin.ld, xp.get(), g->dtype, pp, n, s);
+    Scratch rowsq(sizeof(double) * n * pp.np, s);
+    if (g->dtype == CSC_F64)
+      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), yp.as<double>(), EPI_ROWSQ, rowsq.as<double>(),
+                             n, s);
+    else
+      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), yp.as<float>(), EPI_ROWSQ, rowsq.as<double>(), n,
+                            s);
+    // panel tables for the normaliser
+    std::vector<int> meta(3 * pp.np);
+    for (int j = 0; j < pp.np; ++j) {
+      meta[j] = pp.pw[j];
+      meta[pp.np + j] = pp.wc[j];
+      meta[2 * pp.np + j] = pp.c0[j];
+    }
+    Scratch dmeta(sizeof(int) * meta.size(), s), doff(sizeof(int64_t) * pp.np, s);
+    CSC_CUDA(cudaMemcpyAsync(dmeta.get(), meta.data(), sizeof(int) * meta.size(), cudaMemcpyHostToDevice, s));
+    CSC_CUDA(cudaMemcpyAsync(doff.get(), pp.off.data(), sizeof(int64_t) * pp.np, cudaMemcpyHostToDevice, s));
+    StagedOut fo;
+    stage_out(F, ldf, n, ncols, io_dtype, g->device, s, fo);
+    DeviceOut zo(zero_flags, (size_t)n, g->device, s);
+    Scratch nz(sizeof(unsigned long long), s);
+    CSC_CUDA(cudaMemsetAsync(nz.get(), 0, sizeof(unsigned long long), s));
+    const int* pw = dmeta.as<int>();
+    const int* wc = pw + pp.np;
+    const int* c0 = pw + 2 * pp.np;
+    const int grid = (int)std::min<int64_t>((n + 7) / 8, (int64_t)device_props(g->device).sms * 16);
+    if (g->dtype == CSC_F64 && io_dtype == CSC_F64)
+      k_normalize_rows<double, double><<<grid, 256, 0, s>>>(yp.as<double>(), rowsq.as<double>(), pp.np, pw, wc, c0,
+                                                            doff.as<int64_t>(), n, (double*)fo.p, fo.ld,
+                                                            zo.as<uint8_t>(), nz.as<unsigned long long>());
+    else if (g->dtype == CSC_F32 && io_dtype == CSC_F64)
+      k_normalize_rows<float, double><<<grid, 256, 0, s>>>(yp.as<float>(), rowsq.as<double>(), pp.np, pw, wc, c0,
+                                                           doff.as<int64_t>(), n, (double*)fo.p, fo.ld,
+                                                           zo.as<uint8_t>(), nz.as<unsigned long long>());
+    else if (g->dtype == CSC_F64 && io_dtype == CSC_F32)
+      k_normalize_rows<double, float><<<grid, 256, 0, s>>>(yp.as<double>(), rowsq.as<double>(), pp.np, pw, wc, c0,
+                                                           doff.as<int64_t>(), n, (float*)fo.p, fo.ld,
+                                                           zo.as<uint8_t>(), nz.as<unsigned long long>());
+    else
+      k_normalize_rows<float, float><<<grid, 256, 0, s>>>(yp.as<float>(), rowsq.as<double>(), pp.np, pw, wc, c0,
+                                                          doff.as<int64_t>(), n, (float*)fo.p, fo.ld,
+                                                          zo.as<uint8_t>(), nz.as<unsigned long long>());
+    CSC_LAUNCHED();
+    finish_out(fo, n, ncols, io_dtype, s);
+    zo.finish();
+    unsigned long long hz = 0;
+    CSC_CUDA(cudaMemcpyAsync(&hz, nz.get(), sizeof(hz), cudaMemcpyDeviceToHost, s));
+    CSC_CUDA(cudaStreamSynchronize(s));
+    if (num_zero) *num_zero = (int64_t)hz;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+"""Synthetic stochastic-block-model inputs and the clustering quality metric.
+
+Inputs, not hot path: this module only produces the
+graphs the benchmarks and parity tests run on.  ``sbm_generate`` reproduces the
+reference generator draw for draw (sbm.py:83-155: geometric gap skipping per
+community pair in row-major pair order, strict-upper-triangle unpacking for
+intra-community blocks), so for the same ``SbmConfig`` it yields the same
+graph as the reference; the COO -> canonical CSR step then runs on the device
+(K1).  ``dcsbm_generate`` is the degree-corrected variant BASELINE config 4
+asks for, which the reference does not have.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from .graph import DeviceGraph, Graph
+from . import _lib
+
+__all__ = [
+    "SbmConfig",
+    "adjusted_rand_index",
+    "critical_epsilon",
+    "dcsbm_generate",
+    "sbm_edges",
+    "sbm_generate",
+]
+
+
+@dataclass
+class SbmConfig:
+    num_nodes: int
+    k: int
+    avg_degree: float
+    epsilon: float
+    sizes: list[int] | None = None
+    seed: int = 0
+
+    def __post_init__(self) -> None:
+        if not 0.0 <= self.epsilon <= 1.0:
+            raise ValueError(f"epsilon must lie in [0, 1], got {self.epsilon}")
+        if self.sizes is None:
+            base, extra = divmod(self.num_nodes, self.k)
+            self.sizes = [base + (1 if i < extra else 0) for i in range(self.k)]
+        if len(self.sizes) != self.k:
+            raise ValueError(f"{len(self.sizes)} sizes for k={self.k} communities")
+        if any(s <= 0 for s in self.sizes):
+            raise ValueError("community sizes must be positive")
+        if sum(self.sizes) != self.num_nodes:
+            raise ValueError(f"sizes sum to {sum(self.sizes)}, expected {self.num_nodes}")
+        if not 0.0 < self.q1 <= 1.0:
+            raise ValueError(f"derived q1={self.q1:.4g} outside (0, 1]; lower avg_degree or raise N")
+
+    @property
+    def q1(self) -> float:
+        """Intra-community edge probability s k / (N (1 + eps (k - 1)))."""
+        return self.avg_degree * self.k / (self.num_nodes * (1.0 + self.epsilon * (self.k - 1)))
+
+    @property
+    def q2(self) -> float:
+        return self.epsilon * self.q1
+
+
+def critical_epsilon(avg_degree: float, k: int) -> float:
+    """Detectability threshold (s - sqrt s) / (s + sqrt s (k - 1))."""
+    if avg_degree <= 1:
+        raise ValueError("average degree must exceed 1")
+    r = math.sqrt(avg_degree)
+    return (avg_degree - r) / (avg_degree + r * (k - 1))
+
+
+def _success_positions(cells: int, q: float, rng: np.random.Generator) -> np.ndarray:
+    """Indices of the successes among ``cells`` Bernoulli(q) trials via geometric gaps.
+
+    Batch sizing and the draw sequence match the reference (sbm.py:83-100) so the
+    generator state advances identically.
+    """
+    if cells <= 0 or q <= 0.0:
+        return np.empty(0, dtype=np.int64)
+    if q >= 1.0:
+        return np.arange(cells, dtype=np.int64)
+    mean = q * cells
+    batch = max(64, int(mean + 10.0 * math.sqrt(mean) + 10.0))
+    chunks = []
+    last = -1
+    while last < cells:
+        pos = last + np.cumsum(rng.geometric(q, size=batch))
+        chunks.append(pos)
+        last = int(pos[-1])
+    pos = np.concatenate(chunks)
+    return pos[pos < cells]
+
+
+def _unpack_lower(t: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """t = i(i-1)/2 + j with 0 <= j < i  ->  (i, j), exact for int64 t."""
+    i = ((1.0 + np.sqrt(1.0 + 8.0 * t.astype(np.float64))) / 2.0).astype(np.int64)
+    i = np.where(i * (i - 1) // 2 > t, i - 1, i)
+    i = np.where(i * (i - 1) // 2 + i <= t, i + 1, i)
+    return i, t - i * (i - 1) // 2
+
+
+def sbm_edges(cfg: SbmConfig) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Undirected edge list (each pair once) and ground-truth labels."""
+    rng = np.random.default_rng(cfg.seed)
+    sizes = np.asarray(cfg.sizes, dtype=np.int64)
+    first = np.concatenate([[0], np.cumsum(sizes)])
+    src: list[np.ndarray] = []
+    dst: list[np.ndarray] = []
+    for a in range(cfg.k):
+        for b in range(a, cfg.k):
+            if a == b:
+                pos = _success_positions(int(sizes[a]) * (int(sizes[a]) - 1) // 2, cfg.q1, rng)
+                if pos.size:
+                    i, j = _unpack_lower(pos)
+                    src.append(first[a] + i)
+                    dst.append(first[a] + j)
+            else:
+                pos = _success_positions(int(sizes[a]) * int(sizes[b]), cfg.q2, rng)
+                if pos.size:
+                    src.append(first[a] + pos // sizes[b])
+                    dst.append(first[b] + pos % sizes[b])
+    labels = np.repeat(np.arange(cfg.k), sizes)
+    if not src:
+        return np.empty(0, np.int64), np.empty(0, np.int64), labels
+    return np.concatenate(src), np.concatenate(dst), labels
+
+
+def _device_build(src, dst, num_nodes: int, device: int | None) -> Graph:
+    dev = _lib.default_device() if device is None else int(device)
+    dg = DeviceGraph.from_edges(src, dst, None, num_nodes, "error", _lib.CSC_F64, dev)
+    graph, _ = Graph._from_device(dg)
+    return graph
+
+
+def sbm_generate(cfg: SbmConfig, *, device: int | None = None) -> tuple[Graph, np.ndarray]:
+    """SBM graph (unit weights, nodes ordered by community) and its labels (reference sbm.py:118-155)."""
+    src, dst, labels = sbm_edges(cfg)
+    return _device_build(src, dst, cfg.num_nodes, device), labels
+
+
+def dcsbm_edges(cfg: SbmConfig, pareto_alpha: float = 2.5) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """Degree-corrected SBM edges (BASELINE config 4; not in the reference).
+
+    Propensities theta_i = 1 + Pareto(alpha) (classical Pareto, x_m = 1),
+    normalised to mean 1 within each community.  Edges follow the Poisson
+    (Karrer-Newman) DC-SBM: the number of edges between communities a <= b is
+    Poisson(q_ab * sum_a(theta) * sum_b(theta)) (halved on the diagonal), with
+    endpoints drawn proportionally to theta inside their community, so that
+    P(i~j) ~= theta_i theta_j q_ab and E[deg_i] = theta_i * avg_degree.
+    Loops are dropped and repeated pairs collapse to one unit-weight edge.
+    Expected O(#E log N) work.
+    """
+    rng = np.random.default_rng(cfg.seed)
+    sizes = np.asarray(cfg.sizes, dtype=np.int64)
+    first = np.concatenate([[0], np.cumsum(sizes)])
+    comm = np.repeat(np.arange(cfg.k), sizes)
+    theta = 1.0 + rng.pareto(pareto_alpha, size=cfg.num_nodes)
+    sums = np.add.reduceat(theta, first[:-1])
+    theta = theta / (sums / sizes)[comm]
+    cum = np.cumsum(theta)
+    lo_c = np.concatenate([[0.0], cum])[first[:-1]]
+    hi_c = cum[first[1:] - 1]
+
+    def draw_in(c: np.ndarray) -> np.ndarray:
+        u = lo_c[c] + rng.random(c.size) * (hi_c[c] - lo_c[c])
+        return np.minimum(np.searchsorted(cum, u, side="right"), first[c + 1] - 1)
+
+    # intra-community edges
+    m_intra = rng.poisson(cfg.q1 * sizes.astype(np.float64) ** 2 / 2.0)
+    ca = np.repeat(np.arange(cfg.k), m_intra)
+    i1, j1 = draw_in(ca), draw_in(ca)
+    # inter-community edges: Poisson thinning of a global theta-weighted process
+    m_all = rng.poisson(cfg.q2 * float(cfg.num_nodes) ** 2 / 2.0)
+    u = rng.random(m_all) * cum[-1]
+    v = rng.random(m_all) * cum[-1]
+    i2 = np.minimum(np.searchsorted(cum, u, side="right"), cfg.num_nodes - 1)
+    j2 = np.minimum(np.searchsorted(cum, v, side="right"), cfg.num_nodes - 1)
+    cross = comm[i2] != comm[j2]
+    i = np.concatenate([i1, i2[cross]])
+    j = np.concatenate([j1, j2[cross]])
+    keep = i != j
+    lo, hi = np.minimum(i[keep], j[keep]), np.maximum(i[keep], j[keep])
+    key = np.unique(lo.astype(np.int64) * cfg.num_nodes + hi)
+    return key // cfg.num_nodes, key % cfg.num_nodes, comm, theta
+
+
+def dcsbm_generate(cfg: SbmConfig, pareto_alpha: float = 2.5, *, device: int | None = None):
+    """Degree-corrected SBM graph, labels and propensities (see ``dcsbm_edges``)."""
+    src, dst, labels, theta = dcsbm_edges(cfg, pareto_alpha)
+    return _device_build(src, dst, cfg.num_nodes, device), labels, theta
+
+
+def adjusted_rand_index(labels_a: Sequence[int], labels_b: Sequence[int]) -> float:
+    """Hubert-Arabie ARI from the contingency table (reference sbm.py:158-185)."""
+    a = np.asarray(labels_a)
+    b = np.asarray(labels_b)
+    if a.shape != b.shape or a.ndim != 1:
+        raise ValueError("label vectors must be 1-d and of equal length")
+    n = a.size
+    if n < 2:
+        return 1.0
+    _, ai = np.unique(a, return_inverse=True)
+    _, bi = np.unique(b, return_inverse=True)
+    nb = int(bi.max()) + 1
+    joint = np.bincount(ai * nb + bi, minlength=(int(ai.max()) + 1) * nb).astype(np.float64)
+    pairs = lambda x: float(np.sum(x * (x - 1.0))) / 2.0  # noqa: E731
+    s_ij = pairs(joint)
+    s_a = pairs(np.bincount(ai).astype(np.float64))
+    s_b = pairs(np.bincount(bi).astype(np.float64))
+    expected = s_a * s_b / pairs(float(n))
+    top = 0.5 * (s_a + s_b)
+    if top == expected:
+        return 1.0
+    return (s_ij - expected) / (top - expected)

@@ -1,0 +1,120 @@
+"""Generate the golden fixtures from the REAL reference package.
+
+Run in the build container only (the reference lives at /root/reference and is
+not shipped to the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py [--c2]
+
+Outputs (committed, small): tests/golden/graphs.npz, filter_c1.npz,
+pipeline_c1.npz and, with --c2, pipeline_c2.npz (scalars, indices and labels
+only; the reference takes ~2.5 min there).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+
+import cscluster as ref
+from cscluster._rng import substream, substream_seed
+
+OUT = Path(__file__).resolve().parent
+
+
+def sbm_config(N, k, s=16.0, seed=0):
+    return ref.SbmConfig(num_nodes=N, k=k, avg_degree=s, epsilon=ref.critical_epsilon(s, k) / 4.0, seed=seed)
+
+
+def graphs():
+    out = {}
+    g, truth = ref.sbm_generate(sbm_config(1000, 20))
+    out.update(c1_indptr=g.indptr, c1_indices=g.indices, c1_weights=g.weights, c1_degrees=g.degrees, c1_truth=truth)
+    # messy weighted edge list: same-direction duplicates, reversed duplicates, explicit zeros, isolated tail
+    rng = np.random.default_rng(2024)
+    m = 400
+    src = rng.integers(0, 70, m)
+    dst = rng.integers(0, 70, m)
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    w = np.round(rng.uniform(0.0, 3.0, src.size), 3)
+    w[::17] = 0.0
+    dup = rng.choice(src.size, 60, replace=False)
+    src = np.concatenate([src, src[dup], dst[dup[:30]]])
+    dst = np.concatenate([dst, dst[dup], src[dup[:30]]])
+    w = np.concatenate([w, np.round(rng.uniform(0.0, 2.0, 60), 3), np.round(rng.uniform(0.0, 4.0, 30), 3)])
+    edges = np.column_stack([src, dst, w]).astype(np.float64)
+    gm = ref.build_graph(edges, num_nodes=75)
+    out.update(messy_edges=edges, messy_indptr=gm.indptr, messy_indices=gm.indices, messy_weights=gm.weights,
+               messy_degrees=gm.degrees)
+    # weighted random graph (reference tests/helpers.py random_graph style) + Laplacian apply
+    rng = np.random.default_rng(11)
+    e = [(i, j, rng.uniform(0.2, 2.0)) for i in range(60) for j in range(i + 1, 60) if rng.random() < 0.12]
+    gw = ref.build_graph(e, num_nodes=60)
+    X = np.random.default_rng(12).standard_normal((60, 4))
+    opw = ref.laplacian_op(gw)
+    out.update(w60_edges=np.asarray(e), w60_indptr=gw.indptr, w60_indices=gw.indices, w60_weights=gw.weights,
+               w60_X=X, w60_LX=opw.apply(X), w60_low=ref.apply_filter(ref.design_lowpass(0.9, 30), opw, X))
+    np.savez_compressed(OUT / "graphs.npz", **out)
+
+
+def filter_c1():
+    g, _ = ref.sbm_generate(sbm_config(1000, 20))
+    op = ref.laplacian_op(g)
+    X = np.random.default_rng(1).standard_normal((1000, 28))
+    low = ref.design_lowpass(0.37, 50)
+    high = ref.matched_highpass(low)
+    out = dict(
+        X=X, low_coeffs=low.coeffs, high_coeffs=high.coeffs, Y_low=ref.apply_filter(low, op, X),
+        Y_high=ref.apply_filter(high, op, X), LX=op.apply(X[:, :4]), ridge=ref.psd_ridge(high),
+        Y_order2=ref.apply_filter(ref.design_lowpass(1.3, 2), op, X[:, :5]),
+        Y_order1=ref.apply_filter(ref.design_lowpass(0.8, 1, damping="none"), op, X[:, :3]),
+    )
+    np.savez_compressed(OUT / "filter_c1.npz", **out)
+
+
+def pipeline(N, k, d, seed, full: bool):
+    g, truth = ref.sbm_generate(sbm_config(N, k))
+    op = ref.laplacian_op(g)
+    params = ref.CscParams(k=k, d=d, seed=seed)
+    prm = params.resolve(N)
+    est = ref.estimate_lambda_k(op, k, order=prm.p, rng=substream(seed, "probe"))
+    low = ref.design_lowpass(est.lambda_k_hat, prm.p)
+    sig = ref.generate_signals(N, d, "gaussian", substream(seed, "signals"))
+    feats = ref.build_features(op, low, sig)
+    samp = ref.draw_sampling(N, prm.n, substream(seed, "sampling"), exclude=feats.zero_rows)
+    lab = ref.kmeans(feats.rows[samp.indices], ref.KmeansConfig(k=k, seed=substream_seed(seed, "kmeans")))
+    res = ref.run_csc(op, params)
+    assert res.diagnostics["lambda_k_hat"] == est.lambda_k_hat
+    out = dict(
+        trace=np.asarray(est.trace), lambda_k_hat=est.lambda_k_hat, indices=samp.indices,
+        kmeans_labels=lab.labels, kmeans_inertia=lab.inertia, labels=res.labels, truth=truth,
+        solver_iterations=np.asarray(res.diagnostics["solver_iterations"]),
+        solver_residuals=np.asarray(res.diagnostics["solver_residuals"]), ridge=res.diagnostics["ridge"],
+        zero_rows=feats.zero_rows, result_json=np.frombuffer(res.to_json().encode(), dtype=np.uint8),
+        ari_truth=ref.adjusted_rand_index(truth, res.labels), timings=json.dumps(res.diagnostics["timings"]),
+    )
+    if full:
+        out.update(features=feats.rows, soft=res.soft)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--c2", action="store_true")
+    args = ap.parse_args()
+    graphs()
+    filter_c1()
+    np.savez_compressed(OUT / "pipeline_c1.npz", **pipeline(1000, 20, int(math.ceil(4 * math.log(1000))), 0, True))
+    if args.c2:
+        np.savez_compressed(OUT / "pipeline_c2.npz", **pipeline(100_000, 20, int(math.ceil(4 * math.log(1e5))), 0, False))
+    for p in sorted(OUT.glob("*.npz")):
+        print(p.name, p.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()

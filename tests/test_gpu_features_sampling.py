@@ -1,0 +1,154 @@
+"""Features (filter + row normalisation), block CG and assignment against the reference."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import D_C1, relerr
+from gpu_util import c1_graph, c1_op, options, oracle_csr
+from oracle import cpu_ref as O
+import paper_1602_02018_b200 as P
+from paper_1602_02018_b200._rng import substream
+
+pytestmark = pytest.mark.gpu
+
+
+def c1_features(op, golden):
+    low = P.design_lowpass(float(golden["lambda_k_hat"]), 50)
+    sig = P.generate_signals(1000, D_C1, "gaussian", substream(0, "signals"))
+    return P.build_features(op, low, sig)
+
+
+@pytest.mark.parametrize("rec", [0, 1])
+@pytest.mark.parametrize("pw", [0, 8])
+def test_features_c1_golden(c1_golden, rec, pw):
+    with options(recurrence=rec, panel_width=pw):
+        f = c1_features(c1_op(), c1_golden)
+    assert relerr(f.rows, c1_golden["features"]) <= 1e-9
+    assert np.abs(f.rows - c1_golden["features"]).max() <= 1e-9
+    assert np.array_equal(f.zero_rows, c1_golden["zero_rows"])
+    assert f.normalized and f.provenance["filter"]["order"] == 50
+
+
+def test_features_c1_fp32(c1_golden):
+    f = c1_features(c1_op("float32"), c1_golden)
+    assert relerr(f.rows, c1_golden["features"]) <= 1e-4
+
+
+def test_zero_rows_and_cliques():
+    k3 = P.laplacian_op(P.build_graph([(0, 1, 1.0), (1, 2, 1.0), (0, 2, 1.0)]))
+    ident = P.PolyFilter(coeffs=np.array([1.0]), cutoff=1.0, order=0, damping="none", kind="lowpass")
+    sig = P.generate_signals(3, 4, "gaussian", 0)
+    sig.matrix[1] = 0.0
+    f = P.build_features(k3, ident, sig)
+    assert f.zero_rows.tolist() == [1] and np.all(f.rows[1] == 0.0)
+    assert np.allclose(np.linalg.norm(f.rows[[0, 2]], axis=1), 1.0)
+    edges = [(c * 10 + i, c * 10 + j, 1.0) for c in range(3) for i in range(10) for j in range(i + 1, 10)]
+    op = P.laplacian_op(P.build_graph(edges, num_nodes=30))
+    f = P.build_features(op, P.design_lowpass(0.5, 200), P.generate_signals(30, 8, "gaussian", 0))
+    truth = np.repeat(np.arange(3), 10)
+    for c in range(3):
+        rows = f.rows[truth == c]
+        assert np.abs(rows - rows[0]).max() < 1e-4
+    assert P.pairwise_distance(f, 0, 10) > 0.5
+
+
+def reduced_c1(golden):
+    n = golden["indices"].size
+    red = np.zeros((n, 20))
+    red[np.arange(n), golden["kmeans_labels"]] = 1.0
+    return red
+
+
+@pytest.mark.parametrize("rec", [0, 1])
+def test_block_cg_c1_golden(c1_golden, rec):
+    hp = P.matched_highpass(P.design_lowpass(float(c1_golden["lambda_k_hat"]), 50))
+    cfg = P.InterpolationConfig(highpass=hp)
+    assert cfg.ridge == float(c1_golden["ridge"])
+    samp = P.SamplingSet(indices=c1_golden["indices"], num_nodes=1000)
+    with options(recurrence=rec):
+        X, info = P.interpolate_all(c1_op(), cfg, samp, reduced_c1(c1_golden))
+    assert relerr(X, c1_golden["soft"]) <= 1e-9
+    assert np.array_equal(info.iterations, c1_golden["solver_iterations"])
+    assert np.allclose(info.residuals, c1_golden["solver_residuals"], rtol=1e-6, atol=0)
+    assert bool(np.all(info.converged))
+
+
+def test_block_cg_c1_fp32(c1_golden):
+    hp = P.matched_highpass(P.design_lowpass(float(c1_golden["lambda_k_hat"]), 50))
+    cfg = P.InterpolationConfig(highpass=hp)
+    samp = P.SamplingSet(indices=c1_golden["indices"], num_nodes=1000)
+    X, info = P.interpolate_all(c1_op("float32"), cfg, samp, reduced_c1(c1_golden))
+    assert relerr(X, c1_golden["soft"]) <= 1e-4
+    lab = P.assign(X)
+    assert P.adjusted_rand_index(lab, c1_golden["labels"]) >= 0.99
+
+
+def test_system_apply_vs_oracle():
+    g, _ = c1_graph()
+    hp = P.design_highpass(0.5, 30)
+    cfg = P.InterpolationConfig(highpass=hp)
+    mask = np.zeros(1000)
+    mask[np.random.default_rng(2).choice(1000, 40, replace=False)] = 1.0
+    X = np.random.default_rng(3).standard_normal((1000, 6))
+    ref = O.system_apply(oracle_csr(g), hp.coeffs, cfg.gamma, cfg.ridge, mask, X)
+    assert relerr(P.sampling._system_apply(c1_op(), cfg, mask, X), ref) <= 1e-12
+    q = float(X[:, 0] @ P.sampling._system_apply(c1_op(), cfg, mask, X[:, :1]).ravel())
+    assert q >= -1e-10
+
+
+def test_cg_dense_direct_and_contracts():
+    g, _ = c1_graph()
+    op = c1_op()
+    L = O.dense_laplacian(oracle_csr(g))
+    w, U = np.linalg.eigh(L)
+    cfg = P.InterpolationConfig(highpass=P.design_highpass(0.45, 40), solver_tol=1e-10)
+    samp = P.draw_sampling(1000, 60, 8)
+    c_r = np.random.default_rng(0).standard_normal(60)
+    x, info = P.interpolate(op, cfg, samp, c_r)
+    assert bool(np.all(info.converged))
+    mask = np.zeros(1000)
+    mask[samp.indices] = 1.0
+    A = np.diag(mask) + cfg.gamma * (U @ ((cfg.highpass.evaluate(w) + cfg.ridge)[:, None] * U.T))
+    ref = np.linalg.solve(A, samp.adjoint(c_r))
+    assert np.linalg.norm(x - ref) <= 1e-6 * np.linalg.norm(ref)
+    # zero data -> zero solution, no iterations
+    z, zi = P.interpolate(op, cfg, samp, np.zeros(60))
+    assert np.all(z == 0.0) and zi.max_iterations == 0 and bool(np.all(zi.converged))
+    # non-convergence is flagged, not raised
+    bad = P.InterpolationConfig(highpass=P.design_highpass(0.45, 40), solver_tol=1e-12, solver_max_iters=2)
+    _, bi = P.interpolate(op, bad, samp, c_r)
+    assert not bool(np.all(bi.converged)) and bi.iterations[0] == 2 and bi.residuals[0] > 0
+    with pytest.raises(ValueError):
+        P.interpolate_all(op, cfg, samp, np.zeros((59, 2)))
+
+
+def test_assign_semantics():
+    assert P.assign(np.eye(4)).tolist() == [0, 1, 2, 3]
+    rng = np.random.default_rng(0)
+    soft = np.abs(rng.standard_normal((30, 4)))
+    base = P.assign(soft)
+    assert np.array_equal(P.assign(soft * np.array([3.0, 0.1, 7.5, 1.0])), base)
+    soft = np.eye(3)
+    soft[1] = 0.0
+    lab, info = P.assign(soft, return_info=True)
+    assert lab[1] == 0 and info["fallback_nodes"].tolist() == [1]
+    with pytest.raises(ValueError):
+        P.assign(np.zeros((4, 2)))
+    assert P.assign(np.array([[0.5, 0.5], [0.2, 0.8]])).tolist() == [0, 1]
+    z = np.array([[0.0, 1.0, 0.0], [0.0, 2.0, 0.0], [0.0, 0.5, 0.0]])  # zero-norm columns never win
+    assert P.assign(-z).tolist() == [1, 1, 1]
+    for seed in range(3):
+        soft = np.random.default_rng(seed).standard_normal((5000, 37))
+        assert np.array_equal(P.assign(soft), O.assign(soft)[0])
+
+
+def test_gather_rows(c1_golden):
+    import torch
+
+    from paper_1602_02018_b200.pipeline import _gather_rows
+
+    F = torch.tensor(c1_golden["features"], device="cuda")
+    rows = _gather_rows(F, c1_golden["indices"], 0)
+    assert np.array_equal(rows, c1_golden["features"][c1_golden["indices"]])

@@ -1,0 +1,186 @@
+"""Host-side logic of the drop-in (no GPU): designs, RNG streams, k-means, sampling, params, generators."""
+
+from __future__ import annotations
+
+import re
+
+import numpy as np
+import pytest
+
+from conftest import D_C1, ROOT, c1_config, has_gpu
+from oracle import cpu_ref as O
+import paper_1602_02018_b200 as P
+from paper_1602_02018_b200 import _lib
+from paper_1602_02018_b200._rng import substream, substream_seed
+from paper_1602_02018_b200.features import generate_signals
+from paper_1602_02018_b200.sbm import dcsbm_edges
+
+
+# ---- C ABI surface ----------------------------------------------------------
+
+
+def header_functions() -> list[str]:
+    text = (ROOT / "include" / "csc_b200.h").read_text()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(csc_\w+)\(", text, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = header_functions()
+    assert len(names) >= 19
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.SIGNATURES)
+    assert lib.csc_abi_version() == 1
+
+
+def test_options_roundtrip_and_validation():
+    old = _lib.get_option("panel_width")
+    _lib.set_option("panel_width", 16)
+    assert _lib.get_option("panel_width") == 16
+    _lib.set_option("panel_width", old)
+    with pytest.raises(ValueError):
+        _lib.set_option("recurrence", 7)
+    with pytest.raises(ValueError):
+        _lib.set_option("no_such_knob", 1)
+
+
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
+def test_hot_path_fails_loudly_without_gpu():
+    with pytest.raises(RuntimeError, match="CUDA"):
+        P.build_graph([(0, 1, 1.0)])
+
+
+# ---- filter design (bit-identical coefficients) ------------------------------
+
+
+@pytest.mark.parametrize("cut,order,damp", [(0.37, 50, "jackson"), (1.3, 2, "jackson"), (0.8, 1, "none"),
+                                            (1.999999999999, 50, "jackson")])
+def test_design_matches_oracle(cut, order, damp):
+    low = P.design_lowpass(cut, order, damp)
+    assert np.array_equal(low.coeffs, O.lowpass_coeffs(cut, order, damp))
+    hi = P.matched_highpass(low)
+    assert np.array_equal(hi.coeffs, O.highpass_coeffs(O.lowpass_coeffs(cut, order, damp)))
+    assert P.psd_ridge(hi) == O.psd_ridge(hi.coeffs)
+    grid = np.linspace(0, 2, 301)
+    assert np.array_equal(low.evaluate(grid), O.evaluate(low.coeffs, grid))
+
+
+def test_design_golden(filter_golden):
+    low = P.design_lowpass(0.37, 50)
+    assert np.array_equal(low.coeffs, filter_golden["low_coeffs"])
+    assert P.psd_ridge(P.matched_highpass(low)) == float(filter_golden["ridge"])
+
+
+def test_design_validation_and_json(tmp_path):
+    for bad in (0.0, 2.0):
+        with pytest.raises(ValueError):
+            P.design_lowpass(bad, 10)
+    with pytest.raises(ValueError):
+        P.design_lowpass(1.0, 0)
+    with pytest.raises(ValueError):
+        P.matched_highpass(P.design_highpass(0.5, 10))
+    f = P.design_lowpass(0.7321, 33)
+    f.save(tmp_path / "f.json")
+    g = P.PolyFilter.load(tmp_path / "f.json")
+    assert np.array_equal(g.coeffs, f.coeffs) and g.cutoff == f.cutoff and g.kind == f.kind
+
+
+# ---- random streams, sampling, k-means ----------------------------------------
+
+
+def test_substreams_match_oracle():
+    for stage in ("probe", "signals", "sampling", "kmeans"):
+        a = substream(7, stage).standard_normal(5)
+        b = O.substream(7, stage).standard_normal(5)
+        assert np.array_equal(a, b)
+        assert substream_seed(7, stage) == O.substream_seed(7, stage)
+
+
+def test_signals_and_sampling_match_golden(c1_golden):
+    sig = generate_signals(1000, D_C1, "gaussian", substream(0, "signals"))
+    ref = O.gaussian_signals(1000, D_C1, O.substream(0, "signals"))
+    assert np.array_equal(sig.matrix, ref)
+    s = P.draw_sampling(1000, 120, substream(0, "sampling"), exclude=c1_golden["zero_rows"])
+    assert np.array_equal(s.indices, c1_golden["indices"])
+    with pytest.raises(ValueError):
+        P.draw_sampling(5, 6, 0)
+    with pytest.raises(ValueError):
+        P.draw_sampling(5, 4, 0, exclude=np.arange(3))
+
+
+def test_kmeans_matches_golden(c1_golden):
+    rows = c1_golden["features"][c1_golden["indices"]]
+    lab = P.kmeans(rows, P.KmeansConfig(k=20, seed=substream_seed(0, "kmeans")))
+    assert np.array_equal(lab.labels, c1_golden["kmeans_labels"])
+    assert lab.inertia == float(c1_golden["kmeans_inertia"])
+
+
+def test_kmeans_matches_oracle_random():
+    rng = np.random.default_rng(3)
+    pts = np.concatenate([rng.normal(c, 0.3, (40, 5)) for c in range(6)])
+    a = P.kmeans(pts, P.KmeansConfig(k=6, seed=11, replicates=5))
+    b = O.kmeans(pts, 6, 11, replicates=5)
+    assert np.array_equal(a.labels, b[0]) and a.inertia == b[1] and a.iterations_run == b[2]
+
+
+def test_labels_to_indicators():
+    ind = P.labels_to_indicators(np.array([0, 2, 1, 2]), 3, 4)
+    assert ind.tolist() == [[1, 0, 0], [0, 0, 1], [0, 1, 0], [0, 0, 1]]
+    with pytest.raises(ValueError):
+        P.labels_to_indicators(np.array([0, 3]), 3, 2)
+
+
+# ---- parameters --------------------------------------------------------------
+
+
+def test_params_resolve_and_dict():
+    prm = P.CscParams(k=20).resolve(1000)
+    assert (prm.n, prm.d) == (120, 20)
+    assert P.default_num_samples(3) == 7 and P.default_num_signals(7) == 8
+    with pytest.raises(ValueError, match="n="):
+        P.CscParams(k=5, n=3).resolve(100)
+    with pytest.raises(ValueError, match="k must"):
+        P.CscParams(k=1).resolve(100)
+    with pytest.raises(ValueError, match="exceeds"):
+        P.CscParams(k=3, n=50).resolve(20)
+    with pytest.raises(ValueError, match="gamma"):
+        P.CscParams(k=3, gamma=0.0).resolve(100)
+    p = P.CscParams(k=7, p=80, gamma=2e-3, seed=5)
+    assert P.CscParams.from_dict(p.to_dict()) == p
+    with pytest.raises(ValueError, match="unknown"):
+        P.CscParams.from_dict({"k": 3, "shrink": True})
+
+
+# ---- generators and metric -----------------------------------------------------
+
+
+def test_sbm_config_and_threshold():
+    cfg = c1_config()
+    assert cfg.sizes == [50] * 20
+    assert abs(P.critical_epsilon(16.0, 20) - 12.0 / 92.0) < 1e-15
+    with pytest.raises(ValueError):
+        P.SbmConfig(num_nodes=10, k=2, avg_degree=4.0, epsilon=1.5)
+
+
+def test_dcsbm_degrees_heavy_tailed():
+    cfg = P.SbmConfig(num_nodes=20000, k=20, avg_degree=5.5, epsilon=P.critical_epsilon(5.5, 20) / 4.0, seed=0)
+    src, dst, labels, theta = dcsbm_edges(cfg)
+    assert np.all(src < dst)
+    key = src * cfg.num_nodes + dst
+    assert np.unique(key).size == key.size
+    deg = np.bincount(np.concatenate([src, dst]), minlength=cfg.num_nodes)
+    assert 4.8 < deg.mean() < 6.0
+    assert deg.max() > 8 * deg.mean()  # heavy tail (Pareto 2.5 propensities)
+    for a in range(cfg.k):
+        assert abs(theta[labels == a].mean() - 1.0) < 1e-12
+    intra = (labels[src] == labels[dst]).mean()
+    expect = 1.0 / (1.0 + cfg.epsilon * (cfg.k - 1))
+    assert abs(intra - expect) < 0.03
+
+
+def test_ari():
+    a = np.array([0, 0, 1, 1, 2, 2])
+    assert P.adjusted_rand_index(a, a) == 1.0
+    assert P.adjusted_rand_index(a, np.array([5, 5, 3, 3, 1, 1])) == 1.0
+    assert abs(P.adjusted_rand_index(a, np.array([0, 1, 0, 1, 0, 1]))) < 0.5
