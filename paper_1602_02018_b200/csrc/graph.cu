@@ -11,8 +11,8 @@
 //      of each run (W = max(A, A^T), graph.py:124; absent entries are 0 and all
 //      weights are >= 0, so max over the present ones is the same);
 //   3. drop explicit zeros (graph.py:62), split keys into row/column.
-// Degrees are fp64 row sums taken sequentially in column order, which is the
-// order scipy's csr row sum uses (graph.py:63), so they are bit-identical.
+// Degrees are fp64 row sums in the summation order scipy's CSR row sum uses
+// (np.add.reduceat, graph.py:63), so they are bit-identical.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -30,12 +30,37 @@ inline int grid_for(int64_t work, int threads = kThreads) {
   return static_cast<int>(g);
 }
 
-// degrees, d^-1/2 (graph.py:63, 168)
+// numpy's pairwise summation (the add-reduce inner loop): sequential below 8
+// terms, 8 interleaved accumulators up to 128, halving recursion above.
+__device__ double np_pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
+// degrees and d^-1/2 (graph.py:63, 168).  scipy's CSR row sum is
+// np.add.reduceat(data, indptr), i.e. a[0] + pairwise(a[1:]) per row; the same
+// order here makes the degrees bit-identical for arbitrary weights.
 __global__ void k_degrees(const int32_t* __restrict__ indptr, const double* __restrict__ w, int64_t n,
                           double* __restrict__ deg, double* __restrict__ dis) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int32_t e = indptr[i]; e < indptr[i + 1]; ++e) s += w[e];
+    const int32_t b = indptr[i], e = indptr[i + 1];
+    const double s = e > b ? w[b] + np_pairwise_sum(w + b + 1, e - b - 1) : 0.0;
     deg[i] = s;
     dis[i] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
   }
