@@ -78,14 +78,20 @@ __global__ void k_cg_update(T* __restrict__ X, T* __restrict__ R, const T* __res
   }
 }
 
-// P = R + beta P  (sampling.py:164)
+// P = R + beta P  (sampling.py:164), also written in the filter's scaled basis
+// Ps = D^-1/2 P.  beta == NULL: P = R (initial direction, sampling.py:149).
 template <typename T>
-__global__ void k_cg_direction(T* __restrict__ P, const T* __restrict__ R, const double* __restrict__ beta, int64_t n,
-                               int pw, int wc) {
+__global__ void k_cg_direction(T* __restrict__ P, T* __restrict__ Ps, const T* __restrict__ R,
+                               const double* __restrict__ beta, const double* __restrict__ dis, int64_t n, int pw,
+                               int wc) {
   const int64_t total = n * pw;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(t % pw);
-    if (c < wc) P[t] = static_cast<T>((double)R[t] + beta[c] * (double)P[t]);
+    const int64_t row = t / pw;
+    const int c = (int)(t - row * pw);
+    if (c >= wc) continue;
+    const T p = beta ? static_cast<T>((double)R[t] + beta[c] * (double)P[t]) : R[t];
+    P[t] = p;
+    Ps[t] = static_cast<T>((double)p * dis[row]);
   }
 }
 
@@ -185,7 +191,7 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
               int pw, int wc, T* Xp, double* resid, uint8_t* conv, int64_t* its, int64_t* iters_run, cudaStream_t s) {
   const int64_t N = g->n;
   const size_t pb = sizeof(T) * (size_t)N * pw;
-  Scratch R(pb, s), P(pb, s), AP(pb, s), B0(pb, s), B1(pb, s), Yacc;
+  Scratch R(pb, s), P(pb, s), Ps(pb, s), AP(pb, s), B0(pb, s), B1(pb, s), Yacc;
   if (g_opt.recurrence.load() == 1) Yacc.alloc(pb, s);
   const int cg = colred_grid(g->device);
   const int cap = std::max(step_grid_cap(g->device), cg);
@@ -208,7 +214,11 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
     k_scatter_rhs<T><<<grid, 256, 0, s>>>(reduced, k, idx, n, c0, wc, pw, R.as<T>());
     CSC_LAUNCHED();
   }
-  CSC_CUDA(cudaMemcpyAsync(P.get(), R.get(), pb, cudaMemcpyDeviceToDevice, s));
+  CSC_CUDA(cudaMemsetAsync(P.get(), 0, pb, s));
+  CSC_CUDA(cudaMemsetAsync(Ps.get(), 0, pb, s));
+  const int dgrid = (int)std::max<int64_t>(1, std::min<int64_t>((N * pw + 255) / 256, (int64_t)device_props(g->device).sms * 16));
+  k_cg_direction<T><<<dgrid, 256, 0, s>>>(P.as<T>(), Ps.as<T>(), R.as<T>(), nullptr, g->dis, N, pw, wc);
+  CSC_LAUNCHED();
   k_colsumsq<T><<<cg, 256, 0, s>>>(R.as<T>(), N, pw, wc, part.as<double>());
   CSC_LAUNCHED();
   k_cg_init<<<1, 128, 0, s>>>(part.as<double>(), cg, pw, wc, tol, st);
@@ -227,8 +237,8 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
       ex.gamma = gamma;
       ex.ridge = ridge;
       ex.ap = AP.get();
-      const int fgrid = filter_panel<T>(g, hp, nc, P.as<T>(), nullptr, B0.as<T>(), B1.as<T>(), Yacc.as<T>(), pw, wc,
-                                        EPI_CGAP, ex, s);
+      const int fgrid = filter_panel<T>(g, hp, nc, P.as<T>(), Ps.as<T>(), nullptr, B0.as<T>(), B1.as<T>(),
+                                        Yacc.as<T>(), pw, wc, EPI_CGAP, ex, s);
       k_cg_alpha<<<1, 128, 0, s>>>(part.as<double>(), fgrid, pw, wc, st);
       CSC_LAUNCHED();
       k_cg_update<T><<<cg, 256, 0, s>>>(Xp, R.as<T>(), P.as<T>(), AP.as<T>(), st.alpha, N, pw, wc, part.as<double>());
@@ -236,8 +246,7 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
       ++iters;
       k_cg_beta<<<1, 128, 0, s>>>(part.as<double>(), cg, pw, wc, iters, st);
       CSC_LAUNCHED();
-      const int dgrid = (int)std::min<int64_t>((N * pw + 255) / 256, (int64_t)device_props(g->device).sms * 16);
-      k_cg_direction<T><<<std::max(dgrid, 1), 256, 0, s>>>(P.as<T>(), R.as<T>(), st.beta, N, pw, wc);
+      k_cg_direction<T><<<dgrid, 256, 0, s>>>(P.as<T>(), Ps.as<T>(), R.as<T>(), st.beta, g->dis, N, pw, wc);
       CSC_LAUNCHED();
       CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
       CSC_CUDA(cudaStreamSynchronize(s));

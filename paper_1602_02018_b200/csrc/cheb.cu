@@ -24,6 +24,7 @@ struct Vec16<float> {
     a[3] = v.w;
   }
   __device__ static float4 make(const float (&a)[4]) { return make_float4(a[0], a[1], a[2], a[3]); }
+  __device__ static float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 };
 template <>
 struct Vec16<double> {
@@ -34,45 +35,75 @@ struct Vec16<double> {
     a[1] = v.y;
   }
   __device__ static double2 make(const double (&a)[2]) { return make_double2(a[0], a[1]); }
+  __device__ static double2 zero() { return make_double2(0.0, 0.0); }
 };
 
-template <bool HINT, typename V>
-__device__ __forceinline__ V ld_stream(const V* p) {
-  if constexpr (HINT)
-    return __ldcs(p);  // evict-first: read once per step
-  else
-    return *p;
+template <typename V>
+__device__ __forceinline__ V ld_stream(bool hint, const V* p) {
+  return hint ? __ldcs(p) : *p;  // evict-first: read once per step
 }
-template <bool HINT, typename V>
-__device__ __forceinline__ void st_stream(V* p, const V& v) {
-  if constexpr (HINT)
+template <typename V>
+__device__ __forceinline__ void st_stream(bool hint, V* p, const V& v) {
+  if (hint)
     __stcs(p, v);
   else
     *p = v;
 }
-template <bool HINT, typename S>
-__device__ __forceinline__ S ld_csr(const S* p) {
-  if constexpr (HINT)
-    return __ldcs(p);
-  else
-    return __ldg(p);
+template <typename S>
+__device__ __forceinline__ S ld_csr(bool hint, const S* p) {
+  return hint ? __ldcs(p) : __ldg(p);
 }
 
 // ---------------------------------------------------------------------------
 // The step kernel.  LPR lanes own one row of a panel (VEC elements each);
-// 32/LPR rows per warp; warps stride over row groups.  Each lane keeps U
-// neighbour gathers in flight.
-template <typename T, int LPR, int EPI, bool HINTS, int U>
-__global__ void __launch_bounds__(256) k_cheb_step(const StepArgs a) {
+// 32/LPR rows per warp; warps stride over row groups.
+//
+// Memory-level parallelism is the whole game for this kernel (it streams
+// ~4 N x pw blocks per step and gathers N x deg rows at random), so a row group
+// is processed as:
+//   1. its row-local operands (S, X, row scales) are loaded first, so their
+//      latency overlaps the neighbour gathers;
+//   2. neighbours go in rounds of NB = 16 per row: the row's lanes load the
+//      round's column indices cooperatively (UB = NB/LPR each, coalesced) and
+//      broadcast them with shuffles; the next round's indices are loaded before
+//      the current round's NB independent 16-byte gathers are issued;
+//   3. the next row group's indptr pair is fetched before the epilogue.
+template <int LPR, int CHUNK>
+struct Rounds {
+  static constexpr int NB = LPR > 16 ? LPR : 16;  // neighbours per round per row
+  static constexpr int UB = NB / LPR;             // indices loaded per lane per round
+  static constexpr int CH = CHUNK;                // gathers in flight per lane
+};
+
+template <typename T>
+struct Pair;
+template <>
+struct Pair<float> {
+  using type = float2;
+};
+template <>
+struct Pair<double> {
+  using type = double2;
+};
+
+template <typename T, int LPR, int EPI, int CHUNK, bool UNIT>
+__global__ void __launch_bounds__(256, (CHUNK <= 4 ? 3 : 2)) k_cheb_step(const StepArgs a) {
   using VT = Vec16<T>;
   using V = typename VT::type;
+  using V2 = typename Pair<T>::type;
   constexpr int VEC = VT::n;
   constexpr int PW = LPR * VEC;
   constexpr int GPW = 32 / LPR;
+  constexpr int UB = Rounds<LPR, CHUNK>::UB;
+  constexpr int NB = Rounds<LPR, CHUNK>::NB;
+  constexpr int CH = Rounds<LPR, CHUNK>::CH;
+  const bool HINTS = a.hints != 0;
+  constexpr unsigned FULL = 0xffffffffu;
 
   const int lane = threadIdx.x & 31;
   const int sub = lane % LPR;
   const int grp = lane / LPR;
+  const int gbase = lane & ~(LPR - 1);
   const int col0 = sub * VEC;
   const bool lane_on = col0 < a.wc;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -84,79 +115,165 @@ __global__ void __launch_bounds__(256) k_cheb_step(const StepArgs a) {
   const T* Yin = static_cast<const T*>(a.Yin);
   T* O = static_cast<T*>(a.O);
   T* Y = static_cast<T*>(a.Y);
-  const T* __restrict__ wn = static_cast<const T*>(a.wn);
+  const int32_t* __restrict__ indices = a.indices;
+  const T* __restrict__ wv = static_cast<const T*>(a.wv);
+  const V2* __restrict__ rs = static_cast<const V2*>(a.rs);
   const T ka = static_cast<T>(a.ka), ks = static_cast<T>(a.ks), kx = static_cast<T>(a.kx);
-  const T ky0 = static_cast<T>(a.ky0), ky = static_cast<T>(a.ky);
+  const T ky0 = static_cast<T>(a.ky0), ky = static_cast<T>(a.ky), hz = static_cast<T>(a.hz);
+  const bool last = a.last != 0;
+  const bool sym = last && !a.fwd;  // Clenshaw's last step returns to the symmetric basis
+  const bool want_x = X != nullptr && (a.kx != 0.0 || EPI == EPI_CGAP || last);
 
   double ssq = 0.0;
   double cd[VEC];
 #pragma unroll
   for (int c = 0; c < VEC; ++c) cd[c] = 0.0;
 
-  for (int64_t rb = warp * GPW; rb < a.n; rb += nwarps * GPW) {
+  // row-group schedule: interleaved (warp w takes groups w, w + nwarps, ...) or
+  // contiguous (each warp owns one contiguous run of groups, so an SM works on
+  // neighbouring rows and their shared neighbours can hit in L1)
+  const int64_t ngroups = (a.n + GPW - 1) / GPW;
+  int64_t gfirst, gstep, glast;
+  if (a.contig) {
+    const int64_t per = (ngroups + nwarps - 1) / nwarps;
+    gfirst = warp * per;
+    glast = min(ngroups, gfirst + per);
+    gstep = 1;
+  } else {
+    gfirst = warp;
+    glast = ngroups;
+    gstep = nwarps;
+  }
+  int64_t gi = gfirst;
+  int32_t nbeg = 0, nend = 0;  // indptr pair of the next row group (prefetched)
+  if (G != nullptr && gi < glast && gi * GPW + grp < a.n) {
+    nbeg = __ldg(a.indptr + gi * GPW + grp);
+    nend = __ldg(a.indptr + gi * GPW + grp + 1);
+  }
+  for (; gi < glast; gi += gstep) {
+    const int64_t rb = gi * GPW;
     const int64_t row = rb + grp;
-    const bool on = lane_on && row < a.n;
+    const bool rok = row < a.n;
+    const bool on = rok && lane_on;
+    const int32_t beg = nbeg;
+    const int cnt = nend - nbeg;
+    const size_t off = (size_t)row * PW + col0;
+
+    // 1. row-local operands
+    T sv[VEC], xv[VEC], yv[VEC];
+    V2 sc = {T(0), T(0)};
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) sv[c] = xv[c] = yv[c] = T(0);
+    if (on) {
+      sc = rs[row];
+      if (S != nullptr) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(S + off)), sv);
+      if (want_x) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(X + off)), xv);
+      if (a.fwd) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(Yin + off)), yv);
+    }
+
+    // 2. neighbour rounds
     T acc[VEC];
 #pragma unroll
     for (int c = 0; c < VEC; ++c) acc[c] = T(0);
-
-    if (G != nullptr && on) {
-      const int32_t beg = __ldg(a.indptr + row);
-      const int32_t end = __ldg(a.indptr + row + 1);
-      for (int32_t e = beg; e < end; e += U) {
-        int32_t j[U];
-        T v[U];
+    if (G != nullptr) {
+      const int maxcnt = __reduce_max_sync(FULL, cnt);
+      int32_t jj[UB];
+      T ww[UB];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (e + u < end) {
-            j[u] = ld_csr<HINTS>(a.indices + e + u);
-            v[u] = ld_csr<HINTS>(wn + e + u);
-          } else {
-            j[u] = -1;
-            v[u] = T(0);
+      for (int u = 0; u < UB; ++u) {
+        const int e = u * LPR + sub;
+        jj[u] = e < cnt ? ld_csr(HINTS, indices + beg + e) : -1;
+        if constexpr (!UNIT) ww[u] = e < cnt ? ld_csr(HINTS, wv + beg + e) : T(0);
+      }
+      for (int base = 0; base < maxcnt; base += NB) {
+        int32_t jn[UB];
+        T wn[UB];
+        const bool more = base + NB < maxcnt;  // warp-uniform
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int e = base + NB + u * LPR + sub;
+          jn[u] = (more && e < cnt) ? ld_csr(HINTS, indices + beg + e) : -1;
+          if constexpr (!UNIT) wn[u] = (more && e < cnt) ? ld_csr(HINTS, wv + beg + e) : T(0);
+        }
+        // CH gathers per chunk: broadcast CH indices, issue CH independent loads into
+        // distinct registers, then accumulate in neighbour order (zeros for empty slots)
+#pragma unroll
+        for (int k0 = 0; k0 < NB; k0 += CH) {
+          int32_t jc[CH];
+          T wc[CH];
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            const int slot = k0 + k;  // neighbour slot in this round: held by lane gbase + slot % LPR, entry slot / LPR
+            const int u = slot / LPR, q = slot % LPR;
+            jc[k] = LPR == 1 ? jj[u] : __shfl_sync(FULL, jj[u], gbase + q);
+            wc[k] = T(1);
+            if constexpr (!UNIT) wc[k] = LPR == 1 ? ww[u] : __shfl_sync(FULL, ww[u], gbase + q);
+          }
+          V gv[CH];
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            gv[k] = VT::zero();
+            if (jc[k] >= 0 && lane_on) gv[k] = __ldg(reinterpret_cast<const V*>(G + (size_t)jc[k] * PW + col0));
+          }
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            T g[VEC];
+            VT::unpack(gv[k], g);
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+              if constexpr (UNIT)
+                acc[c] += g[c];
+              else
+                acc[c] = fma(wc[k], g[c], acc[c]);
+            }
           }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (j[u] >= 0) {
-            T gv[VEC];
-            VT::unpack(__ldg(reinterpret_cast<const V*>(G + (size_t)j[u] * PW + col0)), gv);
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) acc[c] = fma(v[u], gv[c], acc[c]);
-          }
+        for (int u = 0; u < UB; ++u) {
+          jj[u] = jn[u];
+          if constexpr (!UNIT) ww[u] = wn[u];
         }
       }
     }
 
+    // 3. prefetch the next row group's indptr pair
+    {
+      const int64_t nrow = (gi + gstep) * GPW + grp;
+      if (G != nullptr && gi + gstep < glast && nrow < a.n) {
+        nbeg = __ldg(a.indptr + nrow);
+        nend = __ldg(a.indptr + nrow + 1);
+      } else {
+        nbeg = nend = 0;
+      }
+    }
+
+    // 4. epilogue
     double rsq = 0.0;
     if (on) {
-      const size_t off = (size_t)row * PW + col0;
-      T out[VEC], xv[VEC], res[VEC];
+      const T si = sc.x, sdi = sc.y;
+      const bool isolated = si == T(0);
+      T out[VEC], res[VEC];
+      const T kacc = ka * (sym ? si : si * si);
+      const T kss = sym ? ks * sdi : ks;
 #pragma unroll
       for (int c = 0; c < VEC; ++c) {
-        out[c] = ka * acc[c];
-        xv[c] = T(0);
+        out[c] = kacc * acc[c];
+        if (S != nullptr) out[c] = fma(kss, sv[c], out[c]);
+        if (want_x) out[c] = fma(kx, xv[c], out[c]);
+        res[c] = out[c];
       }
-      if (S != nullptr) {
-        T sv[VEC];
-        VT::unpack(ld_stream<HINTS>(reinterpret_cast<const V*>(S + off)), sv);
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) out[c] = fma(ks, sv[c], out[c]);
-      }
-      if (X != nullptr) {
-        VT::unpack(ld_stream<HINTS>(reinterpret_cast<const V*>(X + off)), xv);
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) out[c] = fma(kx, xv[c], out[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) res[c] = out[c];
       if (a.fwd) {
-        T yv[VEC];
-        VT::unpack(ld_stream<HINTS>(reinterpret_cast<const V*>(Yin + off)), yv);
 #pragma unroll
-        for (int c = 0; c < VEC; ++c) res[c] = fma(ky, out[c], ky0 * yv[c]);
-        if (Y != nullptr) st_stream<HINTS>(reinterpret_cast<V*>(Y + off), VT::make(res));
+        for (int c = 0; c < VEC; ++c) res[c] = fma(ky, sdi * out[c], ky0 * yv[c]);
       }
+      if (last && isolated) {  // L - I = 0 on an isolated node: Y = h(1) X
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          res[c] = hz * xv[c];
+          if (!a.fwd) out[c] = res[c];
+        }
+      }
+      if (a.fwd && Y != nullptr) st_stream(HINTS, reinterpret_cast<V*>(Y + off), VT::make(res));
       if (O != nullptr) {
         // default write-back: this panel is the next step's gather source, let it stay in L2
         *reinterpret_cast<V*>(O + off) = VT::make(out);
@@ -178,13 +295,13 @@ __global__ void __launch_bounds__(256) k_cheb_step(const StepArgs a) {
           ap[c] = static_cast<T>((double)(m * xv[c]) + gam * reg);
           if (col0 + c < a.wc) cd[c] += (double)xv[c] * (double)ap[c];
         }
-        st_stream<HINTS>(reinterpret_cast<V*>(static_cast<T*>(a.E) + off), VT::make(ap));
+        st_stream(HINTS, reinterpret_cast<V*>(static_cast<T*>(a.E) + off), VT::make(ap));
       }
     }
     if constexpr (EPI == EPI_ROWSQ) {
 #pragma unroll
-      for (int o = LPR / 2; o >= 1; o >>= 1) rsq += __shfl_xor_sync(0xffffffffu, rsq, o);
-      if (sub == 0 && row < a.n) a.part[row] = rsq;
+      for (int o = LPR / 2; o >= 1; o >>= 1) rsq += __shfl_xor_sync(FULL, rsq, o);
+      if (sub == 0 && rok) a.part[row] = rsq;
     }
   }
 
@@ -192,7 +309,7 @@ __global__ void __launch_bounds__(256) k_cheb_step(const StepArgs a) {
   if constexpr (EPI == EPI_SUMSQ) {
     __shared__ double red[32];
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+    for (int o = 16; o >= 1; o >>= 1) ssq += __shfl_xor_sync(FULL, ssq, o);
     if (lane == 0) red[threadIdx.x >> 5] = ssq;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -206,7 +323,7 @@ __global__ void __launch_bounds__(256) k_cheb_step(const StepArgs a) {
 #pragma unroll
     for (int c = 0; c < VEC; ++c) {
 #pragma unroll
-      for (int o = LPR; o < 32; o <<= 1) cd[c] += __shfl_xor_sync(0xffffffffu, cd[c], o);
+      for (int o = LPR; o < 32; o <<= 1) cd[c] += __shfl_xor_sync(FULL, cd[c], o);
     }
     if (grp == 0) {
 #pragma unroll
@@ -214,18 +331,18 @@ __global__ void __launch_bounds__(256) k_cheb_step(const StepArgs a) {
     }
     __syncthreads();
     for (int t = threadIdx.x; t < PW; t += blockDim.x) {
-      double s = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][t];
-      a.part[(size_t)blockIdx.x * PW + t] = s;
+      double sum = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += red[w][t];
+      a.part[(size_t)blockIdx.x * PW + t] = sum;
     }
   }
 }
 
 // ---------------------------------------------------------------------------
 // dispatch
-template <typename T, int LPR, int EPI, bool HINTS, int U>
+template <typename T, int LPR, int EPI, int CHUNK, bool UNIT>
 static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t s) {
-  auto kern = k_cheb_step<T, LPR, EPI, HINTS, U>;
+  auto kern = k_cheb_step<T, LPR, EPI, CHUNK, UNIT>;
   static std::mutex mu;
   static int occ_cache[64] = {0};  // per device
   int occ;
@@ -243,34 +360,56 @@ static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t
   int64_t need = (a.n + rows_per_block - 1) / rows_per_block;
   const int64_t cap = std::min<int64_t>((int64_t)device_props(device).sms * occ, step_grid_cap(device));
   const int grid = (int)std::max<int64_t>(1, std::min(need, cap));
-  kern<<<grid, threads, 0, s>>>(a);
+  const size_t persist = a.G ? persist_bytes(device) : 0;
+  if (persist > 0) {
+    // keep the gathered panel in the persisting L2 set-aside; everything else streams
+    constexpr int VEC = 16 / sizeof(T);
+    const size_t win = std::min<size_t>((size_t)a.n * LPR * VEC * sizeof(T), (size_t)device_props(device).max_window);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(a.G);
+    attr[0].val.accessPolicyWindow.num_bytes = win;
+    attr[0].val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)persist / (double)win));
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CSC_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  } else {
+    kern<<<grid, threads, 0, s>>>(a);
+  }
   CSC_LAUNCHED();
   return grid;
 }
 
-template <typename T, int EPI, bool HINTS, int U>
+template <typename T, int EPI, int CHUNK, bool UNIT>
 static int launch_lpr(const StepArgs& a, int lpr, int threads, int device, cudaStream_t s) {
   switch (lpr) {
-    case 1: return launch_typed<T, 1, EPI, HINTS, U>(a, threads, device, s);
-    case 2: return launch_typed<T, 2, EPI, HINTS, U>(a, threads, device, s);
-    case 4: return launch_typed<T, 4, EPI, HINTS, U>(a, threads, device, s);
-    case 8: return launch_typed<T, 8, EPI, HINTS, U>(a, threads, device, s);
-    case 16: return launch_typed<T, 16, EPI, HINTS, U>(a, threads, device, s);
-    case 32: return launch_typed<T, 32, EPI, HINTS, U>(a, threads, device, s);
+    case 1: return launch_typed<T, 1, EPI, CHUNK, UNIT>(a, threads, device, s);
+    case 2: return launch_typed<T, 2, EPI, CHUNK, UNIT>(a, threads, device, s);
+    case 4: return launch_typed<T, 4, EPI, CHUNK, UNIT>(a, threads, device, s);
+    case 8: return launch_typed<T, 8, EPI, CHUNK, UNIT>(a, threads, device, s);
+    case 16: return launch_typed<T, 16, EPI, CHUNK, UNIT>(a, threads, device, s);
+    case 32: return launch_typed<T, 32, EPI, CHUNK, UNIT>(a, threads, device, s);
   }
   fail(CSC_ERR_INVALID, "unsupported panel width");
 }
 
 template <typename T, int EPI>
 static int launch_epi(const StepArgs& a, int lpr, int threads, int device, cudaStream_t s) {
-  const bool hints = g_opt.cache_hints.load() != 0;
-  const int unroll = (int)g_opt.unroll.load();
-  if (hints) {
-    if (unroll == 4) return launch_lpr<T, EPI, true, 4>(a, lpr, threads, device, s);
-    return launch_lpr<T, EPI, true, 8>(a, lpr, threads, device, s);
+  // UNIT: unit-weight graph, no per-edge values are read
+  const bool chunk4 = g_opt.unroll.load() == 4;
+  const bool unit = a.wv == nullptr;
+  if (chunk4) {
+    if (unit) return launch_lpr<T, EPI, 4, true>(a, lpr, threads, device, s);
+    return launch_lpr<T, EPI, 4, false>(a, lpr, threads, device, s);
   }
-  if (unroll == 4) return launch_lpr<T, EPI, false, 4>(a, lpr, threads, device, s);
-  return launch_lpr<T, EPI, false, 8>(a, lpr, threads, device, s);
+  if (unit) return launch_lpr<T, EPI, 8, true>(a, lpr, threads, device, s);
+  return launch_lpr<T, EPI, 8, false>(a, lpr, threads, device, s);
 }
 
 int step_grid_cap(int device) {
@@ -282,9 +421,11 @@ static double step_bytes(const csc_graph* g, const StepArgs& a, int epi) {
   const double s = (double)dtype_size(g->dtype);
   const double nw = (double)a.n * a.wc * s;
   double b = 0.0;
-  if (a.G) b += 4.0 * (g->n + 1) + (double)g->nnz * (4.0 + s) + nw;  // CSR + one compulsory read of G
+  if (a.G) {  // CSR (indptr + indices [+ weights]) + per-row scales + one compulsory read of G
+    b += 4.0 * (g->n + 1) + (double)g->nnz * (4.0 + (a.wv ? s : 0.0)) + 2.0 * s * a.n + nw;
+  }
   if (a.S) b += nw;
-  if (a.X) b += nw;
+  if (a.X && (a.kx != 0.0 || epi == EPI_CGAP)) b += nw;
   if (a.O) b += nw;
   if (a.fwd) b += nw + (a.Y ? nw : 0.0);
   if (epi == EPI_CGAP) b += nw + (double)a.n;  // AP write + mask
@@ -293,7 +434,10 @@ static double step_bytes(const csc_graph* g, const StepArgs& a, int epi) {
 }
 
 template <typename T>
-int launch_step(const csc_graph* g, const StepArgs& a, int pw, int epi, cudaStream_t s) {
+int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaStream_t s) {
+  StepArgs a = a_in;
+  a.hints = g_opt.cache_hints.load() != 0;
+  a.contig = g_opt.row_order.load() == 1;
   constexpr int VEC = 16 / sizeof(T);
   const int lpr = pw / VEC;
   const int threads = (int)g_opt.block_threads.load();
@@ -317,84 +461,100 @@ template int launch_step<double>(const csc_graph*, const StepArgs&, int, int, cu
 
 // ---------------------------------------------------------------------------
 // filter drivers
+
+// h(1) = sum_l c_l T_l(0), T_l(0) = 1, 0, -1, 0, 1, ...: the filter on an isolated node.
+static double value_at_one(const double* c, int nc) {
+  double h = 0.0;
+  for (int l = 0; l < nc; l += 2) h += ((l / 2) % 2 ? -c[l] : c[l]);
+  return h;
+}
+
 template <typename T>
-int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, T* B0, T* B1, T* Yacc, int pw,
-                 int wc, int epi, const EpiExtra& ex, cudaStream_t s) {
+int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, const T* Xs, T* Y, T* B0, T* B1, T* Yacc,
+                 int pw, int wc, int epi, const EpiExtra& ex, cudaStream_t s) {
   const int p = nc - 1;
+  const double hz = value_at_one(c, nc);
   auto base = [&]() {
     StepArgs a{};
     a.indptr = g->indptr;
     a.indices = g->indices;
-    a.wn = g->wn;
+    a.wv = g->wv;
+    a.rs = g->rs;
     a.n = g->n;
     a.wc = wc;
+    a.hz = hz;
     return a;
   };
-  auto with_epi = [&](StepArgs a, int e) {
-    a.part = ex.part;
+  auto run = [&](StepArgs a, int e) {
+    if (e != EPI_NONE) {
+      a.part = ex.part;
+      a.last = 1;
+    }
     if (e == EPI_CGAP) {
       a.mask = ex.mask;
       a.gamma = ex.gamma;
       a.ridge = ex.ridge;
       a.E = ex.ap;
     }
-    return a;
+    return launch_step<T>(g, a, pw, e, s);
   };
-  auto run = [&](StepArgs a, int e) { return launch_step<T>(g, with_epi(a, e), pw, e, s); };
 
-  if (p == 0) {  // Y = c_0 X  (order 0: filters.py:147 leaves out = c[0] * x)
+  if (p == 0) {  // order 0: Y = c_0 X (filters.py:147)
     StepArgs a = base();
     a.X = X;
     a.kx = c[0];
     a.O = Y;
+    a.last = 1;
     return run(a, epi);
   }
   const bool forward = g_opt.recurrence.load() == 1;
   if (!forward) {
-    // Clenshaw: b_l = c_l X + 2A b_{l+1} - b_{l+2}, A = L - I = -Wn; Y = c_0 X + A b_1 - b_2
+    // Clenshaw: b_l = c_l X + 2A b_{l+1} - b_{l+2}, A = L - I; Y = c_0 X + A b_1 - b_2
     if (p == 1) {
       StepArgs a = base();
-      a.G = X;
+      a.G = Xs;
       a.ka = -c[1];
       a.X = X;
       a.kx = c[0];
       a.O = Y;
+      a.last = 1;
       return run(a, epi);
     }
-    StepArgs a = base();
-    a.G = X;  // b_{p-1} = c_{p-1} X + 2 c_p A X
+    StepArgs a = base();  // b_{p-1} = c_{p-1} X + 2 c_p A X
+    a.G = Xs;
     a.ka = -2.0 * c[p];
-    a.X = X;
+    a.X = Xs;
     a.kx = c[p - 1];
     a.O = B0;
     run(a, EPI_NONE);
-    if (p == 2) {  // Y = c_0 X + A b_1 - b_2, b_2 = c_2 X
+    if (p == 2) {  // Y = c_0 X + A b_1 - b_2 with b_2 = c_2 X
       StepArgs f = base();
       f.G = B0;
       f.ka = -1.0;
       f.X = X;
       f.kx = c[0] - c[2];
       f.O = Y;
+      f.last = 1;
       return run(f, epi);
     }
     StepArgs b = base();  // b_{p-2} = c_{p-2} X + 2A b_{p-1} - c_p X
     b.G = B0;
     b.ka = -2.0;
-    b.X = X;
+    b.X = Xs;
     b.kx = c[p - 2] - c[p];
     b.O = B1;
     run(b, EPI_NONE);
-    T* cur = B1;  // b_{l+1}
-    T* prv = B0;  // b_{l+2}
+    T* cur = B1;  // b~_{l+1}
+    T* prv = B0;  // b~_{l+2}
     for (int l = p - 3; l >= 1; --l) {
       StepArgs m = base();
       m.G = cur;
       m.ka = -2.0;
       m.S = prv;
       m.ks = -1.0;
-      m.X = X;
+      m.X = Xs;
       m.kx = c[l];
-      m.O = prv;  // b_l overwrites b_{l+2} row by row
+      m.O = prv;  // b~_l overwrites b~_{l+2} row by row
       run(m, EPI_NONE);
       std::swap(cur, prv);
     }
@@ -406,16 +566,16 @@ int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, 
     f.X = X;
     f.kx = c[0];
     f.O = Y;
+    f.last = 1;
     return run(f, epi);
   }
 
-  // forward recurrence (filters.py:148-154)
+  // forward recurrence (filters.py:148-154), T~ in the scaled basis, Y symmetric
   T* acc = Y ? Y : Yacc;
   if (!acc) fail(CSC_ERR_INVALID, "forward recurrence needs an accumulator panel");
-  const T* xe = (epi == EPI_CGAP) ? X : nullptr;  // CGAP reads P on the final step
   {
     StepArgs a = base();  // T_1 = (L - I) X;  Y = c_0 X + c_1 T_1
-    a.G = X;
+    a.G = Xs;
     a.ka = -1.0;
     a.O = (p == 1) ? nullptr : B0;
     a.fwd = 1;
@@ -424,14 +584,14 @@ int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, 
     a.ky = c[1];
     a.Y = (p == 1) ? Y : acc;
     if (p == 1) {
-      a.X = xe;
+      a.X = X;  // isolated-node fixup / CGAP operand
+      a.last = 1;
       return run(a, epi);
     }
     run(a, EPI_NONE);
   }
-  const T* t_prev = X;  // T_{l-2}
-  T* t_cur = B0;        // T_{l-1}
-  T* spare = B1;
+  const T* t_prev = Xs;  // T~_{l-2}
+  T* t_cur = B0;         // T~_{l-1}
   for (int l = 2; l <= p; ++l) {
     const bool last = l == p;
     StepArgs a = base();
@@ -439,7 +599,7 @@ int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, 
     a.ka = -2.0;
     a.S = t_prev;
     a.ks = -1.0;
-    T* dst = (t_prev == X) ? spare : const_cast<T*>(t_prev);
+    T* dst = (t_prev == Xs) ? B1 : const_cast<T*>(t_prev);
     a.O = last ? nullptr : dst;
     a.fwd = 1;
     a.Yin = acc;
@@ -447,7 +607,8 @@ int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, 
     a.ky = c[l];
     a.Y = last ? Y : acc;
     if (last) {
-      a.X = xe;
+      a.X = X;
+      a.last = 1;
       return run(a, epi);
     }
     run(a, EPI_NONE);
@@ -457,10 +618,10 @@ int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, 
   return 0;  // unreachable
 }
 
-template int filter_panel<float>(const csc_graph*, const double*, int, const float*, float*, float*, float*, float*,
-                                 int, int, int, const EpiExtra&, cudaStream_t);
-template int filter_panel<double>(const csc_graph*, const double*, int, const double*, double*, double*, double*,
-                                  double*, int, int, int, const EpiExtra&, cudaStream_t);
+template int filter_panel<float>(const csc_graph*, const double*, int, const float*, const float*, float*, float*,
+                                 float*, float*, int, int, int, const EpiExtra&, cudaStream_t);
+template int filter_panel<double>(const csc_graph*, const double*, int, const double*, const double*, double*,
+                                  double*, double*, double*, int, int, int, const EpiExtra&, cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // panels
@@ -507,13 +668,17 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device) {
   return pp;
 }
 
+// one thread per (row, panel column); `scaled` (optional) gets row i times d_i^-1/2
 template <typename Ti, typename To>
-__global__ void k_pack(const Ti* __restrict__ src, int64_t ld, int c0, int wc, int pw, int64_t n, To* __restrict__ dst) {
+__global__ void k_pack(const Ti* __restrict__ src, int64_t ld, int c0, int wc, int pw, int64_t n,
+                       const double* __restrict__ dis, To* __restrict__ dst, To* __restrict__ scaled) {
   const int64_t total = n * pw;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = t / pw;
     const int c = (int)(t - row * pw);
-    dst[t] = c < wc ? static_cast<To>(src[row * ld + c0 + c]) : To(0);
+    const double v = c < wc ? (double)src[row * ld + c0 + c] : 0.0;
+    dst[t] = static_cast<To>(v);
+    if (scaled) scaled[t] = static_cast<To>(v * dis[row]);
   }
 }
 
@@ -532,26 +697,29 @@ static int ew_grid(int64_t work) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64));
 }
 
-void pack_panels(const void* src, int io_dtype, int64_t ld, void* dst, int dtype, const PanelPlan& pp, int64_t n,
-                 cudaStream_t s) {
+template <typename Ti, typename To>
+static void pack_typed(const void* src, int64_t ld, void* dst, void* scaled, const csc_graph* g, const PanelPlan& pp,
+                       cudaStream_t s) {
   for (int j = 0; j < pp.np; ++j) {
-    const int64_t work = n * pp.pw[j];
+    const int64_t work = g->n * pp.pw[j];
     if (work == 0) continue;
-    const int gsz = ew_grid(work);
-    if (io_dtype == CSC_F64 && dtype == CSC_F64)
-      k_pack<double, double><<<gsz, 256, 0, s>>>((const double*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
-                                                 (double*)dst + pp.off[j]);
-    else if (io_dtype == CSC_F64 && dtype == CSC_F32)
-      k_pack<double, float><<<gsz, 256, 0, s>>>((const double*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
-                                                (float*)dst + pp.off[j]);
-    else if (io_dtype == CSC_F32 && dtype == CSC_F64)
-      k_pack<float, double><<<gsz, 256, 0, s>>>((const float*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
-                                                (double*)dst + pp.off[j]);
-    else
-      k_pack<float, float><<<gsz, 256, 0, s>>>((const float*)src, ld, pp.c0[j], pp.wc[j], pp.pw[j], n,
-                                               (float*)dst + pp.off[j]);
+    k_pack<Ti, To><<<ew_grid(work), 256, 0, s>>>(static_cast<const Ti*>(src), ld, pp.c0[j], pp.wc[j], pp.pw[j], g->n,
+                                                 g->dis, static_cast<To*>(dst) + pp.off[j],
+                                                 scaled ? static_cast<To*>(scaled) + pp.off[j] : nullptr);
     CSC_LAUNCHED();
   }
+}
+
+void pack_panels(const void* src, int io_dtype, int64_t ld, void* dst, void* scaled, const csc_graph* g,
+                 const PanelPlan& pp, cudaStream_t s) {
+  if (io_dtype == CSC_F64 && g->dtype == CSC_F64)
+    pack_typed<double, double>(src, ld, dst, scaled, g, pp, s);
+  else if (io_dtype == CSC_F64 && g->dtype == CSC_F32)
+    pack_typed<double, float>(src, ld, dst, scaled, g, pp, s);
+  else if (io_dtype == CSC_F32 && g->dtype == CSC_F64)
+    pack_typed<float, double>(src, ld, dst, scaled, g, pp, s);
+  else
+    pack_typed<float, float>(src, ld, dst, scaled, g, pp, s);
 }
 
 void unpack_panels(const void* src, int dtype, const PanelPlan& pp, int64_t n, void* dst, int io_dtype, int64_t ld,
@@ -579,9 +747,9 @@ void unpack_panels(const void* src, int dtype, const PanelPlan& pp, int64_t n, v
 // fixed-order reductions
 __global__ void k_reduce_sum(const double* __restrict__ in, int64_t count, double* __restrict__ out) {
   __shared__ double red[256];
-  double s = 0.0;
-  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += in[i];
-  red[threadIdx.x] = s;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) acc += in[i];
+  red[threadIdx.x] = acc;
   __syncthreads();
   for (int o = blockDim.x / 2; o >= 1; o >>= 1) {
     if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
@@ -593,9 +761,9 @@ __global__ void k_reduce_sum(const double* __restrict__ in, int64_t count, doubl
 __global__ void k_reduce_cols(const double* __restrict__ in, int64_t nblocks, int stride, int ncols,
                               double* __restrict__ out) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int64_t b = 0; b < nblocks; ++b) s += in[b * stride + c];
-    out[c] = s;
+    double acc = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) acc += in[b * stride + c];
+    out[c] = acc;
   }
 }
 
@@ -609,7 +777,7 @@ void reduce_cols(const double* in, int64_t nblocks, int stride, int ncols, doubl
   CSC_LAUNCHED();
 }
 
-// features: sum panel row-norms in panel order, normalise, flag zero rows
+// features: sum the panel row norms in panel order, normalise, flag zero rows
 template <typename T, typename To>
 __global__ void k_normalize_rows(const T* __restrict__ Yp, const double* __restrict__ rowsq, int np,
                                  const int* __restrict__ pw, const int* __restrict__ wc, const int* __restrict__ c0,
@@ -674,12 +842,6 @@ using namespace csc;
 // C ABI (filter level)
 namespace {
 
-struct BlockIO {
-  int64_t n;
-  int w;
-  int io;
-};
-
 void check_graph(const csc_graph* g) {
   if (!g) fail(CSC_ERR_INVALID, "graph is NULL");
 }
@@ -741,18 +903,43 @@ void finish_out(StagedOut& o, int64_t n, int ncols, int io, cudaStream_t s) {
   CSC_CUDA(cudaMemcpy2DAsync(o.host, es * o.host_ld, o.p, es * ncols, es * ncols, n, cudaMemcpyDeviceToHost, s));
 }
 
+// A row-major input block packed into symmetric and scaled panels.
+struct PackedInput {
+  PanelPlan pp;
+  Scratch x, xs;
+  PackedInput(const csc_graph* g, const void* src, int64_t ld, int ncols, int io, cudaStream_t s) {
+    pp = plan_panels(g->n, ncols, g->dtype, g->device);
+    const size_t cs = dtype_size(g->dtype);
+    StagedIn in;
+    stage_in(src, ld, g->n, ncols, io, g->device, s, in);
+    x.alloc(cs * pp.total, s);
+    xs.alloc(cs * pp.total, s);
+    pack_panels(in.p, io, in.ld, x.get(), xs.get(), g, pp, s);
+  }
+};
+
 template <typename T>
-void run_filter_all(const csc_graph* g, const double* coeffs, int nc, const PanelPlan& pp, const T* Xp, T* Yp,
-                    int epi, double* part, int64_t part_stride, cudaStream_t s) {
+void run_filter_all(const csc_graph* g, const double* coeffs, int nc, const PackedInput& in, T* Yp, int epi,
+                    double* part, int64_t part_stride, cudaStream_t s) {
+  const PanelPlan& pp = in.pp;
   Scratch b0(sizeof(T) * g->n * pp.max_pw, s), b1(sizeof(T) * g->n * pp.max_pw, s);
   Scratch yacc;
   if (!Yp && g_opt.recurrence.load() == 1) yacc.alloc(sizeof(T) * g->n * pp.max_pw, s);
   for (int j = 0; j < pp.np; ++j) {
     EpiExtra ex;
     ex.part = part ? part + part_stride * j : nullptr;
-    filter_panel<T>(g, coeffs, nc, Xp + pp.off[j], Yp ? Yp + pp.off[j] : nullptr, b0.as<T>(), b1.as<T>(),
-                    yacc.as<T>(), pp.pw[j], pp.wc[j], epi, ex, s);
+    filter_panel<T>(g, coeffs, nc, in.x.as<T>() + pp.off[j], in.xs.as<T>() + pp.off[j],
+                    Yp ? Yp + pp.off[j] : nullptr, b0.as<T>(), b1.as<T>(), yacc.as<T>(), pp.pw[j], pp.wc[j], epi, ex, s);
   }
+}
+
+void unpack_out(const csc_graph* g, const PanelPlan& pp, const Scratch& yp, void* Y, int64_t ldy, int ncols, int io,
+                cudaStream_t s) {
+  StagedOut yo;
+  stage_out(Y, ldy, g->n, ncols, io, g->device, s, yo);
+  unpack_panels(yp.get(), g->dtype, pp, g->n, yo.p, io, yo.ld, s);
+  finish_out(yo, g->n, ncols, io, s);
+  if (yo.host) CSC_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace
@@ -769,38 +956,34 @@ int csc_laplacian_apply(const csc_graph* g, const void* X, int64_t ldx, void* Y,
     DeviceGuard dg(g->device);
     ensure_pool(g->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
-    const size_t cs = dtype_size(g->dtype);
-    StagedIn xin;
-    stage_in(X, ldx, g->n, ncols, io_dtype, g->device, s, xin);
-    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s);
-    pack_panels(xin.p, io_dtype, xin.ld, xp.get(), g->dtype, pp, g->n, s);
-    for (int j = 0; j < pp.np; ++j) {  // L X = X - Wn X  (graph.py:154-155)
+    PackedInput in(g, X, ldx, ncols, io_dtype, s);
+    const PanelPlan& pp = in.pp;
+    Scratch yp(dtype_size(g->dtype) * pp.total, s);
+    for (int j = 0; j < pp.np; ++j) {  // L X = X - Wn X  (graph.py:154-155); isolated rows: L x = x
       StepArgs a{};
       a.indptr = g->indptr;
       a.indices = g->indices;
-      a.wn = g->wn;
+      a.wv = g->wv;
+      a.rs = g->rs;
       a.n = g->n;
       a.wc = pp.wc[j];
       a.ka = -1.0;
       a.kx = 1.0;
+      a.hz = 1.0;
+      a.last = 1;
       if (g->dtype == CSC_F64) {
-        a.G = xp.as<double>() + pp.off[j];
-        a.X = a.G;
+        a.G = in.xs.as<double>() + pp.off[j];
+        a.X = in.x.as<double>() + pp.off[j];
         a.O = yp.as<double>() + pp.off[j];
         launch_step<double>(g, a, pp.pw[j], EPI_NONE, s);
       } else {
-        a.G = xp.as<float>() + pp.off[j];
-        a.X = a.G;
+        a.G = in.xs.as<float>() + pp.off[j];
+        a.X = in.x.as<float>() + pp.off[j];
         a.O = yp.as<float>() + pp.off[j];
         launch_step<float>(g, a, pp.pw[j], EPI_NONE, s);
       }
     }
-    StagedOut yo;
-    stage_out(Y, ldy, g->n, ncols, io_dtype, g->device, s, yo);
-    unpack_panels(yp.get(), g->dtype, pp, g->n, yo.p, io_dtype, yo.ld, s);
-    finish_out(yo, g->n, ncols, io_dtype, s);
-    if (yo.host) CSC_CUDA(cudaStreamSynchronize(s));
+    unpack_out(g, pp, yp, Y, ldy, ncols, io_dtype, s);
   });
 }
 
@@ -815,21 +998,13 @@ int csc_cheb_filter(const csc_graph* g, const double* coeffs, int ncoeffs, const
     DeviceGuard dg(g->device);
     ensure_pool(g->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
-    const size_t cs = dtype_size(g->dtype);
-    StagedIn xin;
-    stage_in(X, ldx, g->n, ncols, io_dtype, g->device, s, xin);
-    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s);
-    pack_panels(xin.p, io_dtype, xin.ld, xp.get(), g->dtype, pp, g->n, s);
+    PackedInput in(g, X, ldx, ncols, io_dtype, s);
+    Scratch yp(dtype_size(g->dtype) * in.pp.total, s);
     if (g->dtype == CSC_F64)
-      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), yp.as<double>(), EPI_NONE, nullptr, 0, s);
+      run_filter_all<double>(g, coeffs, ncoeffs, in, yp.as<double>(), EPI_NONE, nullptr, 0, s);
     else
-      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), yp.as<float>(), EPI_NONE, nullptr, 0, s);
-    StagedOut yo;
-    stage_out(Y, ldy, g->n, ncols, io_dtype, g->device, s, yo);
-    unpack_panels(yp.get(), g->dtype, pp, g->n, yo.p, io_dtype, yo.ld, s);
-    finish_out(yo, g->n, ncols, io_dtype, s);
-    if (yo.host) CSC_CUDA(cudaStreamSynchronize(s));
+      run_filter_all<float>(g, coeffs, ncoeffs, in, yp.as<float>(), EPI_NONE, nullptr, 0, s);
+    unpack_out(g, in.pp, yp, Y, ldy, ncols, io_dtype, s);
   });
 }
 
@@ -843,28 +1018,20 @@ int csc_eigencount(const csc_graph* g, const double* coeffs, int ncoeffs, const 
     DeviceGuard dg(g->device);
     ensure_pool(g->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (g->n == 0 || ncols == 0) {
-      DeviceOut co(count, sizeof(double), g->device, s);
-      CSC_CUDA(cudaMemsetAsync(co.as<double>(), 0, sizeof(double), s));
-      co.finish();
-      CSC_CUDA(cudaStreamSynchronize(s));
-      return;
-    }
-    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
-    const size_t cs = dtype_size(g->dtype);
-    StagedIn rin;
-    stage_in(R, ldr, g->n, ncols, io_dtype, g->device, s, rin);
-    Scratch xp(cs * pp.total, s);
-    pack_panels(rin.p, io_dtype, rin.ld, xp.get(), g->dtype, pp, g->n, s);
-    const int cap = step_grid_cap(g->device);
-    Scratch part(sizeof(double) * (size_t)cap * pp.np, s);
-    CSC_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * (size_t)cap * pp.np, s));
-    if (g->dtype == CSC_F64)
-      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), nullptr, EPI_SUMSQ, part.as<double>(), cap, s);
-    else
-      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), nullptr, EPI_SUMSQ, part.as<double>(), cap, s);
     DeviceOut co(count, sizeof(double), g->device, s);
-    reduce_sum(part.as<double>(), (int64_t)cap * pp.np, co.as<double>(), s);
+    if (g->n == 0 || ncols == 0) {
+      CSC_CUDA(cudaMemsetAsync(co.as<double>(), 0, sizeof(double), s));
+    } else {
+      PackedInput in(g, R, ldr, ncols, io_dtype, s);
+      const int cap = step_grid_cap(g->device);
+      Scratch part(sizeof(double) * (size_t)cap * in.pp.np, s);
+      CSC_CUDA(cudaMemsetAsync(part.get(), 0, part.bytes(), s));
+      if (g->dtype == CSC_F64)
+        run_filter_all<double>(g, coeffs, ncoeffs, in, nullptr, EPI_SUMSQ, part.as<double>(), cap, s);
+      else
+        run_filter_all<float>(g, coeffs, ncoeffs, in, nullptr, EPI_SUMSQ, part.as<double>(), cap, s);
+      reduce_sum(part.as<double>(), (int64_t)cap * in.pp.np, co.as<double>(), s);
+    }
     co.finish();
     if (co.on_host()) CSC_CUDA(cudaStreamSynchronize(s));
   });
@@ -886,26 +1053,17 @@ int csc_filter_rowsq(const csc_graph* g, const double* coeffs, int ncoeffs, cons
     DeviceOut ro(rowsq, sizeof(double) * n, g->device, s);
     if (ncols == 0) {
       CSC_CUDA(cudaMemsetAsync(ro.as<double>(), 0, sizeof(double) * n, s));
-      ro.finish();
-      CSC_CUDA(cudaStreamSynchronize(s));
-      return;
+    } else {
+      PackedInput in(g, R, ldr, ncols, io_dtype, s);
+      Scratch yp(dtype_size(g->dtype) * in.pp.total, s), part(sizeof(double) * n * in.pp.np, s);
+      if (g->dtype == CSC_F64)
+        run_filter_all<double>(g, coeffs, ncoeffs, in, yp.as<double>(), EPI_ROWSQ, part.as<double>(), n, s);
+      else
+        run_filter_all<float>(g, coeffs, ncoeffs, in, yp.as<float>(), EPI_ROWSQ, part.as<double>(), n, s);
+      k_sum_panels<<<ew_grid(n), 256, 0, s>>>(part.as<double>(), in.pp.np, n, ro.as<double>());
+      CSC_LAUNCHED();
+      unpack_out(g, in.pp, yp, Y, ldy, ncols, io_dtype, s);
     }
-    const PanelPlan pp = plan_panels(n, ncols, g->dtype, g->device);
-    const size_t cs = dtype_size(g->dtype);
-    StagedIn rin;
-    stage_in(R, ldr, n, ncols, io_dtype, g->device, s, rin);
-    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s), part(sizeof(double) * n * pp.np, s);
-    pack_panels(rin.p, io_dtype, rin.ld, xp.get(), g->dtype, pp, n, s);
-    if (g->dtype == CSC_F64)
-      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), yp.as<double>(), EPI_ROWSQ, part.as<double>(), n, s);
-    else
-      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), yp.as<float>(), EPI_ROWSQ, part.as<double>(), n, s);
-    k_sum_panels<<<ew_grid(n), 256, 0, s>>>(part.as<double>(), pp.np, n, ro.as<double>());
-    CSC_LAUNCHED();
-    StagedOut yo;
-    stage_out(Y, ldy, n, ncols, io_dtype, g->device, s, yo);
-    unpack_panels(yp.get(), g->dtype, pp, n, yo.p, io_dtype, yo.ld, s);
-    finish_out(yo, n, ncols, io_dtype, s);
     ro.finish();
     CSC_CUDA(cudaStreamSynchronize(s));
   });
@@ -915,7 +1073,7 @@ int csc_normalize_rows(const void* Y, int64_t ldy, int64_t num_rows, int ncols, 
                        void* F, int64_t ldf, uint8_t* zero_flags, int64_t* num_zero, int device, void* stream) {
   return guard([&] {
     if (num_rows < 0 || ncols < 0 || ldy < ncols || ldf < ncols) fail(CSC_ERR_INVALID, "bad block shape");
-    const size_t es = dtype_size(io_dtype);
+    dtype_size(io_dtype);
     if (num_rows == 0) {
       if (num_zero) *num_zero = 0;
       return;
@@ -942,7 +1100,6 @@ int csc_normalize_rows(const void* Y, int64_t ldy, int64_t num_rows, int ncols, 
                                                        rq.as<double>(), (float*)fo.p, fo.ld, zo.as<uint8_t>(),
                                                        nz.as<unsigned long long>());
     CSC_LAUNCHED();
-    (void)es;
     finish_out(fo, num_rows, ncols, io_dtype, s);
     zo.finish();
     unsigned long long hz = 0;
@@ -965,13 +1122,11 @@ int csc_system_apply(const csc_graph* g, const double* hp_coeffs, int ncoeffs, d
     DeviceGuard dg(g->device);
     ensure_pool(g->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const PanelPlan pp = plan_panels(g->n, ncols, g->dtype, g->device);
+    PackedInput in(g, X, ldx, ncols, io_dtype, s);
+    const PanelPlan& pp = in.pp;
     const size_t cs = dtype_size(g->dtype);
-    StagedIn xin;
-    stage_in(X, ldx, g->n, ncols, io_dtype, g->device, s, xin);
     DeviceView dm(mask, (size_t)g->n, g->device, s);
-    Scratch xp(cs * pp.total, s), ap(cs * pp.total, s);
-    pack_panels(xin.p, io_dtype, xin.ld, xp.get(), g->dtype, pp, g->n, s);
+    Scratch ap(cs * pp.total, s);
     const int cap = step_grid_cap(g->device);
     Scratch part(sizeof(double) * (size_t)cap * pp.max_pw, s);
     Scratch b0(cs * g->n * pp.max_pw, s), b1(cs * g->n * pp.max_pw, s), yacc;
@@ -984,18 +1139,17 @@ int csc_system_apply(const csc_graph* g, const double* hp_coeffs, int ncoeffs, d
       ex.ridge = ridge;
       if (g->dtype == CSC_F64) {
         ex.ap = ap.as<double>() + pp.off[j];
-        filter_panel<double>(g, hp_coeffs, ncoeffs, xp.as<double>() + pp.off[j], nullptr, b0.as<double>(),
-                             b1.as<double>(), yacc.as<double>(), pp.pw[j], pp.wc[j], EPI_CGAP, ex, s);
+        filter_panel<double>(g, hp_coeffs, ncoeffs, in.x.as<double>() + pp.off[j], in.xs.as<double>() + pp.off[j],
+                             nullptr, b0.as<double>(), b1.as<double>(), yacc.as<double>(), pp.pw[j], pp.wc[j],
+                             EPI_CGAP, ex, s);
       } else {
         ex.ap = ap.as<float>() + pp.off[j];
-        filter_panel<float>(g, hp_coeffs, ncoeffs, xp.as<float>() + pp.off[j], nullptr, b0.as<float>(),
-                            b1.as<float>(), yacc.as<float>(), pp.pw[j], pp.wc[j], EPI_CGAP, ex, s);
+        filter_panel<float>(g, hp_coeffs, ncoeffs, in.x.as<float>() + pp.off[j], in.xs.as<float>() + pp.off[j],
+                            nullptr, b0.as<float>(), b1.as<float>(), yacc.as<float>(), pp.pw[j], pp.wc[j], EPI_CGAP,
+                            ex, s);
       }
     }
-    StagedOut ao;
-    stage_out(AP, ldap, g->n, ncols, io_dtype, g->device, s, ao);
-    unpack_panels(ap.get(), g->dtype, pp, g->n, ao.p, io_dtype, ao.ld, s);
-    finish_out(ao, g->n, ncols, io_dtype, s);
+    unpack_out(g, pp, ap, AP, ldap, ncols, io_dtype, s);
     CSC_CUDA(cudaStreamSynchronize(s));
   });
 }
@@ -1015,19 +1169,13 @@ int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, co
       return;
     }
     const int64_t n = g->n;
-    const PanelPlan pp = plan_panels(n, ncols, g->dtype, g->device);
-    const size_t cs = dtype_size(g->dtype);
-    StagedIn rin;
-    stage_in(R, ldr, n, ncols, io_dtype, g->device, s, rin);
-    Scratch xp(cs * pp.total, s), yp(cs * pp.total, s);
-    pack_panels(rin.p, io_dtype, rin.ld, xp.get(), g->dtype, pp, n, s);
-    Scratch rowsq(sizeof(double) * n * pp.np, s);
+    PackedInput in(g, R, ldr, ncols, io_dtype, s);
+    const PanelPlan& pp = in.pp;
+    Scratch yp(dtype_size(g->dtype) * pp.total, s), rowsq(sizeof(double) * n * pp.np, s);
     if (g->dtype == CSC_F64)
-      run_filter_all<double>(g, coeffs, ncoeffs, pp, xp.as<double>(), yp.as<double>(), EPI_ROWSQ, rowsq.as<double>(),
-                             n, s);
+      run_filter_all<double>(g, coeffs, ncoeffs, in, yp.as<double>(), EPI_ROWSQ, rowsq.as<double>(), n, s);
     else
-      run_filter_all<float>(g, coeffs, ncoeffs, pp, xp.as<float>(), yp.as<float>(), EPI_ROWSQ, rowsq.as<double>(), n,
-                            s);
+      run_filter_all<float>(g, coeffs, ncoeffs, in, yp.as<float>(), EPI_ROWSQ, rowsq.as<double>(), n, s);
     // panel tables for the normaliser
     std::vector<int> meta(3 * pp.np);
     for (int j = 0; j < pp.np; ++j) {

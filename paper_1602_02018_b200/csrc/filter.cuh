@@ -2,13 +2,22 @@
 //
 // Reference: apply_filter (filters.py:140-155) wraps LaplacianOp.apply
 // (graph.py:147-155) in the three-term recurrence T_{l+1} = 2(L-I)T_l - T_{l-1},
-// Y = sum_l c_l T_l.  Here L - I = -Wn with Wn = D^-1/2 W D^-1/2 stored
-// pre-normalized (K1), so one step is one pass over the CSR:
+// Y = sum_l c_l T_l, with L - I = -D^-1/2 W D^-1/2.
 //
-//   out[i,:] = ka * sum_j Wn_ij G[j,:]  +  ks * S[i,:]  +  kx * X[i,:]
-//   (forward mode also)  Y[i,:] = ky0 * Yin[i,:] + ky * out[i,:]
+// Scaled basis.  Every block that is gathered is stored as v~ = D^-1/2 v
+// (s = d^-1/2 per row).  Then  s_i (Wn v)_i = d_i^-1 sum_j w_ij v~_j, i.e. the
+// recurrence runs on the random-walk operator D^-1 W: one step needs the
+// neighbour rows v~_j and, for unit-weight graphs (SBM), nothing per edge but
+// the column index -- no per-edge values, no per-edge scale.  The last step
+// returns to the symmetric basis: (Wn v)_i = s_i sum_j w_ij v~_j and
+// b_i = d_i^{1/2} b~_i.  Isolated nodes (d = 0, where L - I = 0) are fixed up in
+// the last step as Y_i = h(1) X_i (T_l(0) = cos(l pi/2)).
 //
-// with the final step's value optionally reduced in the same pass (epilogues):
+// One step (one pass over the CSR):
+//   mid   out~ = ka d^-1 sum_j w_ij G~_j + ks S~ + kx X~          (scaled -> scaled)
+//   last  out  = ka s   sum_j w_ij G~_j + ks d^{1/2} S~ + kx X     (scaled -> symmetric)
+//   forward mode also  Y = ky0 Yin + ky d^{1/2} out~               (symmetric accumulator)
+// and the last step's value can be reduced in the same pass (epilogues):
 //   SUMSQ  sum of squares (eigencount, spectrum.py:86)
 //   ROWSQ  per-row sum of squares (feature normalisation, features.py:80)
 //   CGAP   AP = mask*P + gamma*(out + ridge*P) and per-column P.AP
@@ -17,10 +26,11 @@
 // Layout: the N x w block is split into column panels (N x pw, row-major within
 // the panel, pw = lanes_per_row * 16B/sizeof(T)).  One node's panel row is one
 // contiguous, 32B-sector-aligned segment, so a neighbour gather is a single
-// coalesced vector load per lane.  A panel is sized to stay L2-resident while it
-// is gathered (the gather is the only non-streaming access); everything else is
-// streamed with evict-first hints.  Filters run panel-major: all p steps of
-// panel 0, then panel 1, ... (columns are independent, filters.py:140).
+// coalesced vector load per lane.  A panel is sized so its gather source can
+// stay L2-resident; filters run panel-major (all p steps of panel 0, then
+// panel 1, ...), columns being independent (filters.py:140).  The lanes of a
+// row load that row's column indices cooperatively and broadcast them with
+// warp shuffles, so the load/store unit mostly issues the 16-byte gathers.
 //
 // Two recurrences are provided:
 //   forward   (north-star kernel): T_{l+1} = -2 Wn T_l - T_{l-1};  Y += c_{l+1} T_{l+1}
@@ -39,20 +49,25 @@ enum Epi : int { EPI_NONE = 0, EPI_SUMSQ = 1, EPI_ROWSQ = 2, EPI_CGAP = 3 };
 struct StepArgs {
   const int32_t* indptr;
   const int32_t* indices;
-  const void* wn;
-  const void* G;    // gathered panel (N x pw); NULL = no SpMM term
-  const void* S;    // same-row stream (may alias O)
-  const void* X;    // same-row stream
+  const void* wv;   // edge weights (compute dtype); NULL for unit-weight graphs
+  const void* rs;   // per-row (d^-1/2, d^1/2)
+  const void* G;    // gathered panel, scaled basis (N x pw); NULL = no SpMM term
+  const void* S;    // same-row stream, scaled basis (may alias O)
+  const void* X;    // same-row stream: scaled X~ on mid steps, symmetric X on last steps
   const void* Yin;  // forward-mode accumulator input (may alias Y)
-  void* O;          // out
+  void* O;          // out (scaled on mid steps, symmetric on the last Clenshaw step)
   void* Y;          // forward-mode accumulator output
   void* E;          // CGAP: AP output
   const uint8_t* mask;  // CGAP: sampling mask
   double* part;     // epilogue partials (SUMSQ [grid], ROWSQ [N], CGAP [grid][pw])
   double ka, ks, kx, ky0, ky, gamma, ridge;
+  double hz;        // h(1) = sum_l c_l T_l(0): value of the filter on isolated nodes
   int64_t n;
-  int wc;   // valid columns in this panel (<= pw)
-  int fwd;  // forward-mode accumulate
+  int wc;        // valid columns in this panel (<= pw)
+  int fwd;       // forward-mode accumulate
+  int last;      // symmetric-basis output + isolated-node fixup (+ epilogue)
+  int hints;     // evict-first hints on streamed operands (set by launch_step)
+  int contig;    // contiguous row ranges per warp (set by launch_step)
 };
 
 struct PanelPlan {
@@ -81,17 +96,20 @@ struct EpiExtra {
   void* ap = nullptr;  // CGAP output panel
 };
 
-// Y = sum_{l<nc} c_l T_l(L - I) X on one panel (X, Y: N x pw).  B0/B1 are N x pw
-// scratch panels; Yacc is needed in forward mode when Y is NULL (SUMSQ/CGAP).
-// Returns the grid used by the final (epilogue) step.
+// Y = sum_{l<nc} c_l T_l(L - I) X on one panel.  X is the symmetric-basis input
+// panel, Xs the same panel in the scaled basis (D^-1/2 X); Y the symmetric-basis
+// output (NULL for SUMSQ/CGAP).  B0/B1 are N x pw scratch panels; Yacc is needed
+// in forward mode when Y is NULL.  Returns the grid of the final (epilogue) step.
 template <typename T>
-int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, T* Y, T* B0, T* B1, T* Yacc, int pw,
-                 int wc, int epi, const EpiExtra& ex, cudaStream_t s);
+int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, const T* Xs, T* Y, T* B0, T* B1, T* Yacc,
+                 int pw, int wc, int epi, const EpiExtra& ex, cudaStream_t s);
 
 // Pack a row-major block (io dtype, leading dim ld) into panels (compute dtype),
-// zero-filling pad columns; unpack is the inverse over valid columns.
-void pack_panels(const void* src, int io_dtype, int64_t ld, void* dst, int dtype, const PanelPlan& pp, int64_t n,
-                 cudaStream_t s);
+// zero-filling pad columns; when `scaled` is non-NULL it also receives the
+// panels in the scaled basis (row i times d_i^-1/2).  Unpack is the inverse of
+// the symmetric pack over valid columns.
+void pack_panels(const void* src, int io_dtype, int64_t ld, void* dst, void* scaled, const csc_graph* g,
+                 const PanelPlan& pp, cudaStream_t s);
 void unpack_panels(const void* src, int dtype, const PanelPlan& pp, int64_t n, void* dst, int io_dtype, int64_t ld,
                    cudaStream_t s);
 

@@ -66,14 +66,21 @@ __global__ void k_degrees(const int32_t* __restrict__ indptr, const double* __re
   }
 }
 
-// Wn_ij = d_i^-1/2 w_ij d_j^-1/2 in the compute dtype.
+// Per-row scales of the scaled-basis recurrence (filter.cuh): (d^-1/2, d^1/2).
 template <typename T>
-__global__ void k_normalize(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                            const double* __restrict__ w, const double* __restrict__ dis, int64_t n,
-                            T* __restrict__ wn) {
+__global__ void k_row_scales(const double* __restrict__ deg, const double* __restrict__ dis, int64_t n,
+                             T* __restrict__ rs) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double di = dis[i];
-    for (int32_t e = indptr[i]; e < indptr[i + 1]; ++e) wn[e] = static_cast<T>(di * w[e] * dis[indices[e]]);
+    rs[2 * i] = static_cast<T>(dis[i]);
+    rs[2 * i + 1] = static_cast<T>(deg[i] > 0.0 ? sqrt(deg[i]) : 0.0);
+  }
+}
+
+template <typename T>
+__global__ void k_cast_weights(const double* __restrict__ w, int64_t nnz, T* __restrict__ out, int* __restrict__ nonunit) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    out[e] = static_cast<T>(w[e]);
+    if (w[e] != 1.0) atomicOr(nonunit, 1);
   }
 }
 
@@ -190,17 +197,39 @@ csc_graph* graph_from_device_csr(int64_t n, int64_t nnz, int32_t* indptr, int32_
     const size_t es = dtype_size(dtype);
     CSC_CUDA(cudaMalloc(&g->degrees, sizeof(double) * (n > 0 ? n : 1)));
     CSC_CUDA(cudaMalloc(&g->dis, sizeof(double) * (n > 0 ? n : 1)));
-    CSC_CUDA(cudaMalloc(&g->wn, es * (nnz > 0 ? nnz : 1)));
+    CSC_CUDA(cudaMalloc(&g->rs, 2 * es * (n > 0 ? n : 1)));
     if (n > 0) {
       k_degrees<<<grid_for(n), kThreads, 0, s>>>(indptr, weights, n, g->degrees, g->dis);
       CSC_LAUNCHED();
       if (dtype == CSC_F64)
-        k_normalize<double><<<grid_for(n), kThreads, 0, s>>>(indptr, indices, weights, g->dis, n,
-                                                              static_cast<double*>(g->wn));
+        k_row_scales<double><<<grid_for(n), kThreads, 0, s>>>(g->degrees, g->dis, n, static_cast<double*>(g->rs));
       else
-        k_normalize<float><<<grid_for(n), kThreads, 0, s>>>(indptr, indices, weights, g->dis, n,
-                                                             static_cast<float*>(g->wn));
+        k_row_scales<float><<<grid_for(n), kThreads, 0, s>>>(g->degrees, g->dis, n, static_cast<float*>(g->rs));
       CSC_LAUNCHED();
+    }
+    // weights in the compute dtype, dropped entirely for unit-weight graphs
+    g->unit = true;
+    if (nnz > 0) {
+      void* wv = nullptr;
+      CSC_CUDA(cudaMalloc(&wv, es * nnz));
+      int* flag = nullptr;
+      CSC_CUDA(cudaMalloc(&flag, sizeof(int)));
+      CSC_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+      if (dtype == CSC_F64)
+        k_cast_weights<double><<<grid_for(nnz), kThreads, 0, s>>>(weights, nnz, static_cast<double*>(wv), flag);
+      else
+        k_cast_weights<float><<<grid_for(nnz), kThreads, 0, s>>>(weights, nnz, static_cast<float*>(wv), flag);
+      CSC_LAUNCHED();
+      int nonunit = 0;
+      CSC_CUDA(cudaMemcpyAsync(&nonunit, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CSC_CUDA(cudaStreamSynchronize(s));
+      cudaFree(flag);
+      if (nonunit) {
+        g->wv = wv;
+        g->unit = false;
+      } else {
+        cudaFree(wv);
+      }
     }
     CSC_CUDA(cudaStreamSynchronize(s));
   } catch (...) {
@@ -216,7 +245,8 @@ void graph_free(csc_graph* g) {
   cudaFree(g->indptr);
   cudaFree(g->indices);
   cudaFree(g->weights);
-  cudaFree(g->wn);
+  cudaFree(g->wv);
+  cudaFree(g->rs);
   cudaFree(g->degrees);
   cudaFree(g->dis);
   delete g;

@@ -70,7 +70,9 @@ struct Options {
   std::atomic<int64_t> block_threads{256};
   std::atomic<int64_t> profile{0};
   std::atomic<int64_t> l2_budget_pct{50}; // auto panel width: panel gather buffer <= pct% of L2
-  std::atomic<int64_t> unroll{8};         // neighbours in flight per lane (4 or 8)
+  std::atomic<int64_t> unroll{8};         // neighbour gathers in flight per lane (4 or 8)
+  std::atomic<int64_t> row_order{0};      // 0 interleaved row groups, 1 contiguous ranges per warp
+  std::atomic<int64_t> l2_persist_pct{0}; // >0: keep the gathered panel in a persisting L2 window
 };
 extern Options g_opt;
 
@@ -100,7 +102,11 @@ struct DeviceGuard {
 struct DeviceProps {
   int sms = 0;
   int l2_bytes = 0;
+  int max_persist = 0;  // cudaDevAttrMaxPersistingL2CacheSize
+  int max_window = 0;   // cudaDevAttrMaxAccessPolicyWindowSize
 };
+// Persisting-L2 set-aside (bytes) configured on `dev` for the current option; 0 if off/unsupported.
+size_t persist_bytes(int dev);
 const DeviceProps& device_props(int dev);
 void ensure_pool(int dev);  // keep freed stream-ordered memory cached
 
@@ -209,9 +215,11 @@ struct csc_graph {
   int32_t* indptr = nullptr;   // [n+1]
   int32_t* indices = nullptr;  // [nnz], strictly increasing per row
   double* weights = nullptr;   // [nnz] original W (fp64), for export
-  void* wn = nullptr;          // [nnz] D^-1/2 W D^-1/2 in the compute dtype
+  void* wv = nullptr;          // [nnz] W in the compute dtype; NULL when every weight is 1 (unit graph)
+  void* rs = nullptr;          // [2n] per-row (d^-1/2, d^1/2) in the compute dtype (0, 0 where d == 0)
   double* degrees = nullptr;   // [n] row sums
   double* dis = nullptr;       // [n] d^-1/2 (0 where d == 0)
+  bool unit = false;
 };
 
 namespace csc {

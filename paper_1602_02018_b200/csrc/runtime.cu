@@ -73,7 +73,30 @@ const DeviceProps& device_props(int dev) {
   DeviceProps p;
   CSC_CUDA(cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev));
   CSC_CUDA(cudaDeviceGetAttribute(&p.l2_bytes, cudaDevAttrL2CacheSize, dev));
+  if (cudaDeviceGetAttribute(&p.max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess) p.max_persist = 0;
+  if (cudaDeviceGetAttribute(&p.max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess) p.max_window = 0;
+  cudaGetLastError();
   return g_props.emplace(dev, p).first->second;
+}
+
+static std::unordered_map<int, int64_t> g_persist_pct;
+static std::unordered_map<int, size_t> g_persist_bytes;
+
+size_t persist_bytes(int dev) {
+  const int64_t pct = g_opt.l2_persist_pct.load();
+  const DeviceProps& p = device_props(dev);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_persist_pct.find(dev);
+  if (it != g_persist_pct.end() && it->second == pct) return g_persist_bytes[dev];
+  size_t want = pct > 0 ? (size_t)((double)p.l2_bytes * (double)pct / 100.0) : 0;
+  if (want > (size_t)p.max_persist) want = (size_t)p.max_persist;
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+    cudaGetLastError();
+    want = 0;
+  }
+  g_persist_pct[dev] = pct;
+  g_persist_bytes[dev] = want;
+  return want;
 }
 
 void ensure_pool(int dev) {
@@ -129,6 +152,8 @@ static std::atomic<int64_t>* option_slot(const char* key) {
   if (k == "profile") return &g_opt.profile;
   if (k == "l2_budget_pct") return &g_opt.l2_budget_pct;
   if (k == "unroll") return &g_opt.unroll;
+  if (k == "l2_persist_pct") return &g_opt.l2_persist_pct;
+  if (k == "row_order") return &g_opt.row_order;
   return nullptr;
 }
 
@@ -142,6 +167,7 @@ int csc_set_option(const char* key, int64_t value) {
       fail(CSC_ERR_INVALID, "block_threads must be a multiple of 32 in [64, 256]");
     if (k == "panel_width" && value < 0) fail(CSC_ERR_INVALID, "panel_width must be >= 0");
     if (k == "unroll" && value != 4 && value != 8) fail(CSC_ERR_INVALID, "unroll must be 4 or 8");
+    if (k == "l2_persist_pct" && (value < 0 || value > 100)) fail(CSC_ERR_INVALID, "l2_persist_pct in [0, 100]");
     if (k == "l2_budget_pct" && (value < 1 || value > 100)) fail(CSC_ERR_INVALID, "l2_budget_pct in [1, 100]");
     slot->store(value);
   });

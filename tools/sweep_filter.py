@@ -43,6 +43,9 @@ def main():
     F = torch.empty_like(X)
     filt = P.design_lowpass(0.43, P_ORDER)
     work = filter_bytes(N, int(g.indices.size), d, 4 if dtype == "float32" else 8, P_ORDER)
+    props = torch.cuda.get_device_properties(0)
+    print(f"device {props.name} L2 {getattr(props, 'L2_cache_size', 0) / 2**20:.0f} MiB, N={N} d={d} {dtype} "
+          f"nnz={int(g.indices.size)}", flush=True)
     combos = [c for c in args.combos.split(";") if c.strip()] or [""]
     for combo in combos:
         old = {}
