@@ -70,7 +70,7 @@ struct Options {
   std::atomic<int64_t> block_threads{256};
   std::atomic<int64_t> profile{0};
   std::atomic<int64_t> l2_budget_pct{50}; // auto panel width: panel gather buffer <= pct% of L2
-  std::atomic<int64_t> unroll{8};         // neighbour gathers in flight per lane (4 or 8)
+  std::atomic<int64_t> unroll{4};         // neighbour gathers in flight per lane (4 or 8)
   std::atomic<int64_t> row_order{0};      // 0 interleaved row groups, 1 contiguous ranges per warp
   std::atomic<int64_t> l2_persist_pct{0}; // >0: keep the gathered panel in a persisting L2 window
 };
