@@ -152,7 +152,7 @@ int csc_gather_rows(const void* F, int64_t ldf, int64_t num_rows, int ncols, int
       k_gather<float><<<grid, 256, 0, s>>>(dF.as<float>(), ldf, ncols, didx.as<int64_t>(), n, num_rows,
                                            static_cast<float*>(dst), ld, bad.as<int>());
     CSC_LAUNCHED();
-    if (!odev) CSC_CUDA(cudaMemcpy2DAsync(out, es * ldo, dst, es * ncols, es * ncols, n, cudaMemcpyDeviceToHost, s));
+    if (!odev) copy_rows(out, ldo, dst, ncols, n, ncols, es, cudaMemcpyDeviceToHost, s);
     int hb = 0;
     CSC_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     CSC_CUDA(cudaStreamSynchronize(s));

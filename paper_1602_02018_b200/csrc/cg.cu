@@ -340,7 +340,7 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
       }
       unpack_panels(xp.get(), g->dtype, pp, N, xdst, io_dtype, xld, s);
       if (!xdev)
-        CSC_CUDA(cudaMemcpy2DAsync(X_out, es * ldx, xs.get(), es * k, es * k, N, cudaMemcpyDeviceToHost, s));
+        copy_rows(X_out, ldx, xs.get(), k, N, k, es, cudaMemcpyDeviceToHost, s);
       CSC_CUDA(cudaStreamSynchronize(s));
     }
     oit.finish();

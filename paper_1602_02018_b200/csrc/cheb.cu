@@ -872,7 +872,7 @@ void stage_in(const void* src, int64_t ld, int64_t n, int ncols, int io, int dev
     return;
   }
   out.buf.alloc(es * n * ncols, s);
-  CSC_CUDA(cudaMemcpy2DAsync(out.buf.get(), es * ncols, src, es * ld, es * ncols, n, cudaMemcpyHostToDevice, s));
+  copy_rows(out.buf.get(), ncols, src, ld, n, ncols, es, cudaMemcpyHostToDevice, s);
   out.p = out.buf.get();
   out.ld = ncols;
 }
@@ -899,8 +899,7 @@ void stage_out(void* dst, int64_t ld, int64_t n, int ncols, int io, int device, 
 }
 void finish_out(StagedOut& o, int64_t n, int ncols, int io, cudaStream_t s) {
   if (!o.host) return;
-  const size_t es = dtype_size(io);
-  CSC_CUDA(cudaMemcpy2DAsync(o.host, es * o.host_ld, o.p, es * ncols, es * ncols, n, cudaMemcpyDeviceToHost, s));
+  copy_rows(o.host, o.host_ld, o.p, ncols, n, ncols, dtype_size(io), cudaMemcpyDeviceToHost, s);
 }
 
 // A row-major input block packed into symmetric and scaled panels.

@@ -151,6 +151,19 @@ inline size_t dtype_size(int dt) {
   fail(CSC_ERR_INVALID, "unknown dtype " + std::to_string(dt));
 }
 
+// Copy n rows of `cols` elements between row-major buffers with leading dims
+// dld/sld.  Dense blocks go as one flat copy (a 2D copy with 10^6 short rows
+// runs far below link speed).
+inline void copy_rows(void* dst, int64_t dld, const void* src, int64_t sld, int64_t n, int64_t cols, size_t es,
+                      cudaMemcpyKind kind, cudaStream_t s) {
+  if (n <= 0 || cols <= 0) return;
+  if (dld == cols && sld == cols) {
+    CSC_CUDA(cudaMemcpyAsync(dst, src, es * n * cols, kind, s));
+  } else {
+    CSC_CUDA(cudaMemcpy2DAsync(dst, es * dld, src, es * sld, es * cols, n, kind, s));
+  }
+}
+
 // A device copy of a (possibly host) input buffer; passes device pointers through.
 class DeviceView {
  public:
