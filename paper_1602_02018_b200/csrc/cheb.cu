@@ -63,16 +63,16 @@ __device__ __forceinline__ S ld_csr(bool hint, const S* p) {
 // is processed as:
 //   1. its row-local operands (S, X, row scales) are loaded first, so their
 //      latency overlaps the neighbour gathers;
-//   2. neighbours go in rounds of NB = 16 per row: the row's lanes load the
-//      round's column indices cooperatively (UB = NB/LPR each, coalesced) and
-//      broadcast them with shuffles; the next round's indices are loaded before
-//      the current round's NB independent 16-byte gathers are issued;
+//   2. neighbours go in chunks of CH = max(LPR, 4|8) per row: the row's lanes
+//      load the chunk's column indices cooperatively (CH/LPR each, coalesced)
+//      and broadcast them with shuffles; the next chunk's indices are loaded
+//      before this chunk's CH independent 16-byte gathers are issued.  Chunks
+//      run to the warp's largest degree, so short rows waste < CH slots;
 //   3. the next row group's indptr pair is fetched before the epilogue.
 template <int LPR, int CHUNK>
 struct Rounds {
-  static constexpr int NB = LPR > 16 ? LPR : 16;  // neighbours per round per row
-  static constexpr int UB = NB / LPR;             // indices loaded per lane per round
-  static constexpr int CH = CHUNK;                // gathers in flight per lane
+  static constexpr int CH = LPR > CHUNK ? LPR : CHUNK;  // neighbours per chunk (= gathers in flight per lane)
+  static constexpr int UC = CH / LPR;                   // indices held per lane per chunk
 };
 
 template <typename T>
@@ -87,16 +87,15 @@ struct Pair<double> {
 };
 
 template <typename T, int LPR, int EPI, int CHUNK, bool UNIT>
-__global__ void __launch_bounds__(256, (CHUNK <= 4 ? 3 : 2)) k_cheb_step(const StepArgs a) {
+__global__ void __launch_bounds__(256, (CHUNK <= 4 ? 4 : 2)) k_cheb_step(const StepArgs a) {
   using VT = Vec16<T>;
   using V = typename VT::type;
   using V2 = typename Pair<T>::type;
   constexpr int VEC = VT::n;
   constexpr int PW = LPR * VEC;
   constexpr int GPW = 32 / LPR;
-  constexpr int UB = Rounds<LPR, CHUNK>::UB;
-  constexpr int NB = Rounds<LPR, CHUNK>::NB;
   constexpr int CH = Rounds<LPR, CHUNK>::CH;
+  constexpr int UC = Rounds<LPR, CHUNK>::UC;
   const bool HINTS = a.hints != 0;
   constexpr unsigned FULL = 0xffffffffu;
 
@@ -171,65 +170,59 @@ __global__ void __launch_bounds__(256, (CHUNK <= 4 ? 3 : 2)) k_cheb_step(const S
       if (a.fwd) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(Yin + off)), yv);
     }
 
-    // 2. neighbour rounds
+    // 2. neighbour chunks: CH neighbours per chunk (the row's lanes hold UC
+    //    indices each), next chunk's indices loaded before this chunk's gathers
     T acc[VEC];
 #pragma unroll
     for (int c = 0; c < VEC; ++c) acc[c] = T(0);
     if (G != nullptr) {
       const int maxcnt = __reduce_max_sync(FULL, cnt);
-      int32_t jj[UB];
-      T ww[UB];
+      int32_t jj[UC];
+      T ww[UC];
 #pragma unroll
-      for (int u = 0; u < UB; ++u) {
+      for (int u = 0; u < UC; ++u) {
         const int e = u * LPR + sub;
         jj[u] = e < cnt ? ld_csr(HINTS, indices + beg + e) : -1;
         if constexpr (!UNIT) ww[u] = e < cnt ? ld_csr(HINTS, wv + beg + e) : T(0);
       }
-      for (int base = 0; base < maxcnt; base += NB) {
-        int32_t jn[UB];
-        T wn[UB];
-        const bool more = base + NB < maxcnt;  // warp-uniform
+      for (int base = 0; base < maxcnt; base += CH) {
+        int32_t jn[UC];
+        T wn[UC];
+        const bool more = base + CH < maxcnt;  // warp-uniform
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
-          const int e = base + NB + u * LPR + sub;
+        for (int u = 0; u < UC; ++u) {
+          const int e = base + CH + u * LPR + sub;
           jn[u] = (more && e < cnt) ? ld_csr(HINTS, indices + beg + e) : -1;
           if constexpr (!UNIT) wn[u] = (more && e < cnt) ? ld_csr(HINTS, wv + beg + e) : T(0);
         }
-        // CH gathers per chunk: broadcast CH indices, issue CH independent loads into
-        // distinct registers, then accumulate in neighbour order (zeros for empty slots)
+        int32_t jc[CH];
+        T wc[CH];
 #pragma unroll
-        for (int k0 = 0; k0 < NB; k0 += CH) {
-          int32_t jc[CH];
-          T wc[CH];
+        for (int k = 0; k < CH; ++k) {  // slot k is entry k / LPR of lane gbase + k % LPR
+          jc[k] = LPR == 1 ? jj[k] : __shfl_sync(FULL, jj[k / LPR], gbase + k % LPR);
+          wc[k] = T(1);
+          if constexpr (!UNIT) wc[k] = LPR == 1 ? ww[k] : __shfl_sync(FULL, ww[k / LPR], gbase + k % LPR);
+        }
+        V gv[CH];
 #pragma unroll
-          for (int k = 0; k < CH; ++k) {
-            const int slot = k0 + k;  // neighbour slot in this round: held by lane gbase + slot % LPR, entry slot / LPR
-            const int u = slot / LPR, q = slot % LPR;
-            jc[k] = LPR == 1 ? jj[u] : __shfl_sync(FULL, jj[u], gbase + q);
-            wc[k] = T(1);
-            if constexpr (!UNIT) wc[k] = LPR == 1 ? ww[u] : __shfl_sync(FULL, ww[u], gbase + q);
-          }
-          V gv[CH];
+        for (int k = 0; k < CH; ++k) {
+          gv[k] = VT::zero();
+          if (jc[k] >= 0 && lane_on) gv[k] = __ldg(reinterpret_cast<const V*>(G + (size_t)jc[k] * PW + col0));
+        }
 #pragma unroll
-          for (int k = 0; k < CH; ++k) {
-            gv[k] = VT::zero();
-            if (jc[k] >= 0 && lane_on) gv[k] = __ldg(reinterpret_cast<const V*>(G + (size_t)jc[k] * PW + col0));
-          }
+        for (int k = 0; k < CH; ++k) {
+          T g[VEC];
+          VT::unpack(gv[k], g);
 #pragma unroll
-          for (int k = 0; k < CH; ++k) {
-            T g[VEC];
-            VT::unpack(gv[k], g);
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-              if constexpr (UNIT)
-                acc[c] += g[c];
-              else
-                acc[c] = fma(wc[k], g[c], acc[c]);
-            }
+          for (int c = 0; c < VEC; ++c) {
+            if constexpr (UNIT)
+              acc[c] += g[c];
+            else
+              acc[c] = fma(wc[k], g[c], acc[c]);
           }
         }
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
+        for (int u = 0; u < UC; ++u) {
           jj[u] = jn[u];
           if constexpr (!UNIT) ww[u] = wn[u];
         }
