@@ -199,7 +199,7 @@ def run_ours(args, cfg):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    grp = Group.current()
+    grp = Group.current()  # column shards: each rank owns d signal columns of a (d x world)-column job
     N, k, s = cfg["N"], cfg["k"], cfg["s"]
     d = int(math.ceil(4 * math.log(N)))
     scfg = P.SbmConfig(num_nodes=N, k=k, avg_degree=s, epsilon=P.critical_epsilon(s, k) / 4.0, seed=0)
@@ -284,8 +284,9 @@ def run_ours(args, cfg):
         if world == 1:
             build_features(op, filt, signals, out=rows_out)
         else:
-            Fl, _ = sharded_features(backend, filt, torch.from_numpy(host).to(f"cuda:{local}"), grp)
-            rows_out[:] = Fl.cpu().numpy()
+            Xh = torch.from_numpy(host).to(f"cuda:{local}").to(dtype_t)
+            Fl, _ = sharded_features(backend, filt, Xh, grp)
+            torch.from_numpy(rows_out).copy_(Fl)
 
     for _ in range(max(1, args.warmup)):
         step_e2e()

@@ -165,6 +165,15 @@ int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int ncoeffs, doubl
 int csc_assign(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dtype, int64_t* labels,
                uint8_t* fallback, int64_t* num_fallback, int device, void* stream);
 
+/* Column-sharded assign: for this rank's columns [col_offset, col_offset + k) of
+ * the soft indicators, per row the best normalised value (fp64, -inf if every
+ * local column has zero norm), its global column (int64) and whether any local
+ * entry is nonzero (uint8).  Ranks merge with the lowest-column tie rule of
+ * sampling.py:210-217.  *any_norm receives 1 if some local column is nonzero. */
+int csc_assign_partial(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dtype, int64_t col_offset,
+                       double* best_val, int64_t* best_col, uint8_t* nonzero, int* any_norm, int device,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,61 @@ __global__ void k_argmax(const T* __restrict__ A, int64_t ld, int64_t n, int k, 
   }
 }
 
+// column-sharded variant: per-row (best value, global column, any nonzero)
+template <typename T>
+__global__ void k_argmax_partial(const T* __restrict__ A, int64_t ld, int64_t n, int k, const double* __restrict__ norm,
+                                 int64_t col_offset, double* __restrict__ bval, int64_t* __restrict__ bcol,
+                                 uint8_t* __restrict__ nz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += nw) {
+    double best = -INFINITY;
+    int bidx = -1;
+    bool nonzero = false;
+    for (int c = lane; c < k; c += 32) {
+      const double v = (double)A[r * ld + c];
+      nonzero |= v != 0.0;
+      const double q = norm[c] > 0.0 ? v / norm[c] : -INFINITY;
+      if (bidx < 0 || q > best) {
+        best = q;
+        bidx = c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (oi >= 0 && (bidx < 0 || ob > best || (ob == best && oi < bidx))) {
+        best = ob;
+        bidx = oi;
+      }
+    }
+    const bool any = __any_sync(0xffffffffu, nonzero);
+    if (lane == 0) {
+      bval[r] = best;
+      bcol[r] = col_offset + bidx;
+      nz[r] = any ? 1 : 0;
+    }
+  }
+}
+
+template <typename T>
+void assign_partial_typed(const T* A, int64_t ld, int64_t n, int k, int device, int64_t col_offset, double* bval,
+                          int64_t* bcol, uint8_t* nz, int* any_norm, cudaStream_t s) {
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)device_props(device).sms * 4));
+  Scratch part(sizeof(double) * (size_t)nb * k, s), norm(sizeof(double) * k, s), flag(sizeof(int), s);
+  CSC_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+  k_colsq_rows<T><<<nb, 256, 0, s>>>(A, ld, n, k, part.as<double>());
+  CSC_LAUNCHED();
+  k_colnorm<<<(k + 127) / 128, 128, 0, s>>>(part.as<double>(), nb, k, norm.as<double>(), flag.as<int>());
+  CSC_LAUNCHED();
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)device_props(device).sms * 16));
+  k_argmax_partial<T><<<grid, 256, 0, s>>>(A, ld, n, k, norm.as<double>(), col_offset, bval, bcol, nz);
+  CSC_LAUNCHED();
+  CSC_CUDA(cudaMemcpyAsync(any_norm, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+}
+
 template <typename T>
 void assign_typed(const T* A, int64_t ld, int64_t n, int k, int device, int64_t* labels, uint8_t* fb,
                   unsigned long long* nfb, cudaStream_t s) {
@@ -187,6 +242,40 @@ int csc_assign(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dty
     CSC_CUDA(cudaMemcpyAsync(&h, nfb.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     CSC_CUDA(cudaStreamSynchronize(s));
     if (num_fallback) *num_fallback = (int64_t)h;
+  });
+}
+
+int csc_assign_partial(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dtype, int64_t col_offset,
+                       double* best_val, int64_t* best_col, uint8_t* nonzero, int* any_norm, int device,
+                       void* stream) {
+  return guard([&] {
+    if (k < 1 || num_rows < 0 || ld < k) fail(CSC_ERR_INVALID, "soft indicators must be (N, k)");
+    if (col_offset < 0) fail(CSC_ERR_INVALID, "col_offset must be >= 0");
+    const size_t es = dtype_size(io_dtype);
+    if (num_rows == 0) {
+      if (any_norm) *any_norm = 0;
+      return;
+    }
+    if (!soft || !best_val || !best_col || !nonzero) fail(CSC_ERR_INVALID, "NULL buffer");
+    DeviceGuard dg(device);
+    ensure_pool(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DeviceView dA(soft, es * (size_t)num_rows * ld, device, s);
+    DeviceOut bv(best_val, sizeof(double) * num_rows, device, s);
+    DeviceOut bc(best_col, sizeof(int64_t) * num_rows, device, s);
+    DeviceOut nzo(nonzero, (size_t)num_rows, device, s);
+    int h_any = 0;
+    if (io_dtype == CSC_F64)
+      assign_partial_typed<double>(dA.as<double>(), ld, num_rows, k, device, col_offset, bv.as<double>(),
+                                   bc.as<int64_t>(), nzo.as<uint8_t>(), &h_any, s);
+    else
+      assign_partial_typed<float>(dA.as<float>(), ld, num_rows, k, device, col_offset, bv.as<double>(),
+                                  bc.as<int64_t>(), nzo.as<uint8_t>(), &h_any, s);
+    bv.finish();
+    bc.finish();
+    nzo.finish();
+    CSC_CUDA(cudaStreamSynchronize(s));
+    if (any_norm) *any_norm = h_any;
   });
 }
 

@@ -5,28 +5,41 @@ spectrum.py:86 sums over columns, sampling.py:133-135 is per-column CG), so the
 graph is replicated and ranks own contiguous slices of the signal / indicator
 columns.  The only exchanges are small:
 
-  eigencount   per-rank partial counts, all-gathered and summed in rank order
-  features     per-rank row sums of squares (N fp64), all-gathered and summed
-               in rank order, then each rank normalises its own columns
-  gather       the n sampled rows of each rank's columns, all-gathered
-  assign       per-row (best value, global column) pairs, all-gathered and
-               merged with the reference's lowest-index tie rule
+  eigencount   per-rank partial counts (1 fp64), all-gathered, summed in rank order
+  features     per-rank row sums of squares (N fp64), all-gathered and summed in
+               rank order, then each rank normalises its own columns
+  gather       the n sampled rows of each rank's columns (n x d_r), all-gathered
+  CG           none per iteration; per-column diagnostics all-gathered at the end
+  assign       per-row (best normalised value, global column, nonzero) triples,
+               all-gathered and merged with the reference's lowest-index tie rule
 
 Sums are taken in rank order on every rank, so results do not depend on the
-collective's internal reduction order.  The per-rank compute goes through a
-backend object (``DeviceBackend`` = the C ABI on this rank's GPU); tests swap in
-a CPU backend to exercise the exchange logic with the gloo backend.
+collective's internal reduction order.  Random draws stay the reference's: every
+rank draws the full probe / signal block from the same named numpy substream and
+keeps its column slice, so the sharded run sees exactly the single-GPU inputs.
+
+Per-rank compute goes through a backend (``DeviceBackend`` = the C ABI on the
+rank's GPU).  Tests plug in a CPU backend built on the oracle to exercise the
+exchange logic with the gloo backend.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import math
+import time
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
-from .filters import PolyFilter, coeff_array
+from ._rng import substream
+from ._signals import normal_block
+from .filters import PolyFilter, coeff_array, design_lowpass, matched_highpass
+from .kmeans import kmeans, labels_to_indicators
+from .result import ClusterResult
+from .sampling import CgInfo, InterpolationConfig, SamplingSet, draw_sampling
+from .spectrum import default_num_signals, round_half_up
 
 
 def column_slice(ncols: int, world: int, rank: int) -> slice:
@@ -36,107 +49,156 @@ def column_slice(ncols: int, world: int, rank: int) -> slice:
     return slice(start, start + base + (1 if rank < extra else 0))
 
 
+@dataclass
+class Group:
+    """A torch.distributed process group plus this rank's position and comm device."""
+
+    rank: int
+    world: int
+    group: object = None
+    device: object = "cpu"
+
+    @classmethod
+    def current(cls, group=None) -> "Group":
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_available() or not dist.is_initialized():
+            return cls(0, 1, None, "cpu")
+        dev = "cpu"
+        if dist.get_backend(group) == "nccl":
+            dev = torch.device("cuda", torch.cuda.current_device())
+        return cls(dist.get_rank(group), dist.get_world_size(group), group, dev)
+
+    def _t(self, a):
+        import torch
+
+        if isinstance(a, torch.Tensor):
+            return a.contiguous().to(self.device)
+        return torch.as_tensor(np.ascontiguousarray(a)).to(self.device)
+
+    def all_gather(self, a):
+        """All ranks' copies of an equally-shaped array (numpy in -> numpy out,
+        tensor in -> tensors on the communication device), in rank order."""
+        if self.world == 1:
+            return [a if not isinstance(a, np.ndarray) else np.asarray(a)]
+        import torch
+        import torch.distributed as dist
+
+        t = self._t(a)
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t, group=self.group)
+        if isinstance(a, torch.Tensor):
+            return [p.to(a.device) for p in parts]
+        return [p.cpu().numpy() for p in parts]
+
+    def all_gather_var(self, a: np.ndarray) -> list[np.ndarray]:
+        """All-gather arrays whose first-axis lengths differ per rank."""
+        if self.world == 1:
+            return [np.asarray(a)]
+        a = np.asarray(a)
+        lens = [int(x[0]) for x in self.all_gather(np.array([a.shape[0]], dtype=np.int64))]
+        top = max(lens)
+        pad = np.zeros((top,) + a.shape[1:], dtype=a.dtype)
+        pad[: a.shape[0]] = a
+        return [p[:n] for p, n in zip(self.all_gather(pad), lens)]
+
+    def sum_in_order(self, a: np.ndarray) -> np.ndarray:
+        """Sum over ranks, accumulated in rank order (deterministic)."""
+        parts = self.all_gather(a)
+        total = parts[0].clone() if hasattr(parts[0], "clone") else parts[0].copy()
+        for p in parts[1:]:
+            total = total + p
+        return total
+
+
 class DeviceBackend:
-    """Per-rank compute on the rank's GPU through the C ABI (inputs/outputs are CUDA tensors)."""
+    """Per-rank compute on the rank's GPU through the C ABI (host numpy in/out, device-resident blocks)."""
 
     def __init__(self, op):
-        self.op = op
+        import torch
 
-    def filter_rowsq(self, filt: PolyFilter, R):
+        self.op = op
+        self.dev = torch.device("cuda", op.device)
+        self.stream = lambda: _lib.current_stream(op.device)
+
+    def _dev(self, a):
+        import torch
+
+        if isinstance(a, torch.Tensor) and a.is_cuda:
+            return a.contiguous()
+        return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
+
+    def count(self, filt: PolyFilter, R: np.ndarray) -> float:
+        if R.shape[1] == 0:
+            return 0.0
+        c = coeff_array(filt)
+        Rd = np.ascontiguousarray(R, dtype=np.float64)
+        out = C.c_double(0.0)
+        _lib.call("csc_eigencount", self.op.handle, _lib.ptr(c), int(c.size), _lib.ptr(Rd), int(Rd.shape[1]),
+                  int(Rd.shape[1]), _lib.CSC_F64, C.byref(out), self.stream())
+        return float(out.value)
+
+    def filter_rowsq(self, filt: PolyFilter, R: np.ndarray):
         import torch
 
         c = coeff_array(filt)
-        Y = torch.empty_like(R)
-        rowsq = torch.empty(R.shape[0], dtype=torch.float64, device=R.device)
-        _lib.call("csc_filter_rowsq", self.op.handle, _lib.ptr(c), int(c.size), R.data_ptr(), int(R.stride(0)),
-                  int(R.shape[1]), _lib.dtype_code(R.dtype), Y.data_ptr(), int(Y.stride(0)), rowsq.data_ptr(),
-                  _lib.current_stream(self.op.device))
-        return Y, rowsq
+        Rd = self._dev(R)
+        Y = torch.empty_like(Rd)
+        rowsq = torch.zeros(R.shape[0], dtype=torch.float64, device=self.dev)
+        if R.shape[1]:
+            _lib.call("csc_filter_rowsq", self.op.handle, _lib.ptr(c), int(c.size), Rd.data_ptr(), int(Rd.shape[1]),
+                      int(Rd.shape[1]), _lib.dtype_code(Rd.dtype), Y.data_ptr(), int(Y.shape[1]), rowsq.data_ptr(),
+                      self.stream())
+        return Y, rowsq  # stays on the device; the group sums it over NCCL
 
     def normalize(self, Y, rowsq):
         import torch
 
         F = torch.empty_like(Y)
-        flags = torch.zeros(Y.shape[0], dtype=torch.uint8, device=Y.device)
+        flags = torch.zeros(Y.shape[0], dtype=torch.uint8, device=self.dev)
         nz = C.c_int64(0)
-        _lib.call("csc_normalize_rows", Y.data_ptr(), int(Y.stride(0)), int(Y.shape[0]), int(Y.shape[1]),
-                  _lib.dtype_code(Y.dtype), rowsq.data_ptr(), F.data_ptr(), int(F.stride(0)), flags.data_ptr(),
-                  C.byref(nz), self.op.device, _lib.current_stream(self.op.device))
-        zero = torch.nonzero(flags).flatten().cpu().numpy() if nz.value else np.empty(0, dtype=np.int64)
-        return F, zero
+        rq = self._dev(rowsq)
+        if Y.shape[1]:
+            _lib.call("csc_normalize_rows", Y.data_ptr(), int(Y.shape[1]), int(Y.shape[0]), int(Y.shape[1]),
+                      _lib.dtype_code(Y.dtype), rq.data_ptr(), F.data_ptr(), int(F.shape[1]), flags.data_ptr(),
+                      C.byref(nz), self.op.device, self.stream())
+            zero = flags.nonzero().flatten().cpu().numpy() if nz.value else np.empty(0, dtype=np.int64)
+        else:
+            zero = np.flatnonzero(rq.cpu().numpy() <= 0.0)
+        return F, zero.astype(np.int64)
 
-    def count(self, filt: PolyFilter, R) -> float:
-        c = coeff_array(filt)
-        out = C.c_double(0.0)
-        _lib.call("csc_eigencount", self.op.handle, _lib.ptr(c), int(c.size), R.data_ptr(), int(R.stride(0)),
-                  int(R.shape[1]), _lib.dtype_code(R.dtype), C.byref(out), _lib.current_stream(self.op.device))
-        return float(out.value)
+    def gather(self, F, idx: np.ndarray) -> np.ndarray:
+        from .pipeline import _gather_rows
 
-    def zeros(self, n, dtype="float64"):
+        if F.shape[1] == 0:
+            return np.zeros((idx.size, 0))
+        return _gather_rows(F, idx, self.op.device)
+
+    def block_cg(self, cfg: InterpolationConfig, sampling: SamplingSet, reduced: np.ndarray):
         import torch
 
-        return torch.zeros(n, dtype=getattr(torch, dtype), device=f"cuda:{self.op.device}")
+        from .sampling import block_cg_into
+
+        X = torch.empty((self.op.num_nodes, reduced.shape[1]), dtype=torch.float64, device=self.dev)
+        if reduced.shape[1] == 0:
+            return X, CgInfo(np.zeros(0, np.int64), np.zeros(0), np.zeros(0, bool))
+        return X, block_cg_into(self.op, cfg, sampling, reduced, X)
+
+    def row_best(self, soft, col0: int):
+        N, k = int(soft.shape[0]), int(soft.shape[1])
+        val = np.full(N, -np.inf)
+        col = np.zeros(N, dtype=np.int64)
+        nz = np.zeros(N, dtype=np.uint8)
+        any_norm = C.c_int(0)
+        if k:
+            _lib.call("csc_assign_partial", soft.data_ptr(), int(soft.stride(0)), N, k, _lib.CSC_F64, int(col0),
+                      _lib.ptr(val), _lib.ptr(col), _lib.ptr(nz), C.byref(any_norm), self.op.device, self.stream())
+        return val, col, nz.astype(bool), bool(any_norm.value)
 
 
-@dataclass
-class Group:
-    """The torch.distributed group plus this rank's position."""
-
-    rank: int
-    world: int
-    group: object = None
-
-    @classmethod
-    def current(cls, group=None) -> "Group":
-        import torch.distributed as dist
-
-        if not dist.is_available() or not dist.is_initialized():
-            return cls(0, 1, None)
-        return cls(dist.get_rank(group), dist.get_world_size(group), group)
-
-    def gather_sum(self, x):
-        """Sum of ``x`` (tensor) over ranks, accumulated in rank order (deterministic)."""
-        import torch
-        import torch.distributed as dist
-
-        if self.world == 1:
-            return x
-        parts = [torch.empty_like(x) for _ in range(self.world)]
-        dist.all_gather(parts, x.contiguous(), group=self.group)
-        total = parts[0].clone()
-        for p in parts[1:]:
-            total += p
-        return total
-
-    def all_gather(self, x):
-        import torch
-        import torch.distributed as dist
-
-        if self.world == 1:
-            return [x]
-        parts = [torch.empty_like(x) for _ in range(self.world)]
-        dist.all_gather(parts, x.contiguous(), group=self.group)
-        return parts
-
-
-def sharded_features(backend, filt: PolyFilter, R_local, grp: Group):
-    """Features for this rank's signal columns, normalised by the global row norms."""
-    Y, rowsq = backend.filter_rowsq(filt, R_local)
-    total = grp.gather_sum(rowsq)
-    return backend.normalize(Y, total)
-
-
-def sharded_count(backend, filt: PolyFilter, R_local, grp: Group) -> float:
-    """Eigencount over all ranks' probe columns (spectrum.py:86)."""
-    import torch
-
-    local = backend.count(filt, R_local)
-    t = torch.tensor([local], dtype=torch.float64, device=getattr(R_local, "device", "cpu"))
-    return float(grp.gather_sum(t).item())
-
-
-def merge_argmax(values: np.ndarray, columns: np.ndarray) -> np.ndarray:
-    """Per-row winner over rank candidates (ranks x N): larger value, ties -> lower column."""
+def merge_argmax(values: list[np.ndarray], columns: list[np.ndarray]) -> np.ndarray:
+    """Per-row winner over rank candidates: larger value, ties -> lower column (sampling.py:210-213)."""
     best_v = values[0].copy()
     best_c = columns[0].copy()
     for v, c in zip(values[1:], columns[1:]):
@@ -144,3 +206,113 @@ def merge_argmax(values: np.ndarray, columns: np.ndarray) -> np.ndarray:
         best_v = np.where(take, v, best_v)
         best_c = np.where(take, c, best_c)
     return best_c
+
+
+def sharded_count(backend, filt: PolyFilter, R_local: np.ndarray, grp: Group) -> float:
+    """Eigencount over all ranks' probe columns (spectrum.py:86)."""
+    return float(grp.sum_in_order(np.array([backend.count(filt, R_local)]))[0])
+
+
+def sharded_features(backend, filt: PolyFilter, R_local, grp: Group):
+    """This rank's feature columns, normalised by the global row norms (features.py:79-87)."""
+    Y, rowsq = backend.filter_rowsq(filt, R_local)
+    return backend.normalize(Y, grp.sum_in_order(rowsq))
+
+
+def sharded_assign(backend, soft_local, col0: int, grp: Group):
+    """Global argmax labels from column-sharded soft indicators (sampling.py:197-220)."""
+    val, col, nz, any_norm = backend.row_best(soft_local, col0)
+    if not any(bool(x[0]) for x in grp.all_gather(np.array([any_norm]))):
+        raise ValueError("all indicator vectors are zero")
+    labels = merge_argmax(grp.all_gather(val), grp.all_gather(col))
+    nonzero = np.zeros(val.size, dtype=bool)
+    for part in grp.all_gather(nz):
+        nonzero |= part.astype(bool)
+    fallback = np.flatnonzero(~nonzero)
+    labels[fallback] = 0  # raw argmax of an all-zero row
+    return labels.astype(np.int64), fallback
+
+
+def estimate_lambda_k_sharded(backend, N: int, k: int, order: int, ds: int | None, rng, grp: Group,
+                              max_steps: int = 20, refine: bool = False):
+    """Dichotomy of spectrum.py:90-140 with the probe columns sharded over ranks."""
+    ds = ds if ds is not None else default_num_signals(N)
+    cols = column_slice(ds, grp.world, grp.rank)
+    lo, hi = 0.0, 2.0
+    trace: list[tuple[float, float]] = []
+
+    def probe(lam):
+        filt = design_lowpass(min(lam, 2.0 - 1e-12), order, damping="jackson")
+        block = normal_block(rng, N, ds)  # every rank draws the full block: identical stream
+        cnt = sharded_count(backend, filt, np.ascontiguousarray(block[:, cols]), grp)
+        trace.append((float(lam), cnt))
+        return cnt
+
+    for _ in range(max_steps):
+        mid = 0.5 * (lo + hi)
+        r = round_half_up(probe(mid))
+        if r == k:
+            lam = mid
+            if refine and (hi - lo) > 0.01 and round_half_up(probe(0.5 * (lo + mid))) == k:
+                lam = 0.5 * (lo + mid)
+            return lam, trace, False
+        if r > k:
+            hi = mid
+        else:
+            lo = mid
+    return 0.5 * (lo + hi), trace, True
+
+
+def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResult:
+    """run_csc (pipeline.py:113-225) with signal and indicator columns sharded over ranks."""
+    N = num_nodes
+    prm = params.resolve(N)
+    t_run = time.perf_counter()
+    warnings: list[str] = []
+    if prm.lambda_k is not None:
+        lam, trace, warn, source = float(prm.lambda_k), [], False, "override"
+    else:
+        lam, trace, warn = estimate_lambda_k_sharded(backend, N, prm.k, prm.p, prm.probe_signals,
+                                                     substream(prm.seed, "probe"), grp, prm.probe_max_steps,
+                                                     prm.probe_refine)
+        source = "estimated"
+        if warn:
+            warnings.append("lambda_k bracket fallback")
+    low = design_lowpass(lam, prm.p, damping=prm.damping)
+    high = matched_highpass(low)
+    dcols = column_slice(prm.d, grp.world, grp.rank)
+    signals = normal_block(substream(prm.seed, "signals"), N, prm.d)
+    F, zero_rows = sharded_features(backend, low, np.ascontiguousarray(signals[:, dcols]), grp)
+    del signals
+    if zero_rows.size:
+        warnings.append(f"{zero_rows.size} zero-norm feature rows")
+    sampling = draw_sampling(N, prm.n, substream(prm.seed, "sampling"), exclude=zero_rows)
+    rows = np.concatenate(grp.all_gather(backend.gather(F, sampling.indices)), axis=1)
+    labeling = kmeans(rows, prm.kmeans)
+    counts = np.bincount(labeling.labels, minlength=prm.k)
+    if np.any(counts == 0):
+        from .pipeline import DegenerateClusteringError
+
+        raise DegenerateClusteringError(f"empty cluster(s) {np.flatnonzero(counts == 0).tolist()} in the reduced k-means")
+    reduced = labels_to_indicators(labeling.labels, prm.k, prm.n)
+    icfg = InterpolationConfig(highpass=high, gamma=prm.gamma, solver_tol=prm.solver_tol,
+                               solver_max_iters=prm.solver_max_iters)
+    kcols = column_slice(prm.k, grp.world, grp.rank)
+    X, info = backend.block_cg(icfg, sampling, np.ascontiguousarray(reduced[:, kcols]))
+    labels, fallback = sharded_assign(backend, X, kcols.start, grp)
+    its = np.concatenate(grp.all_gather_var(info.iterations))
+    res = np.concatenate(grp.all_gather_var(info.residuals))
+    conv = np.concatenate(grp.all_gather_var(info.converged.astype(np.uint8))).astype(bool)
+    if not bool(np.all(conv)):
+        warnings.append("interpolation solver did not reach tolerance")
+    diagnostics = {
+        "method": "csc", "num_nodes": N, "k": prm.k, "n": prm.n, "d": prm.d, "p": prm.p, "gamma": prm.gamma,
+        "seed": prm.seed, "lambda_k_hat": lam, "lambda_source": source, "lambda_warning": warn,
+        "probe_iterations": len(trace), "kmeans_inertia": labeling.inertia,
+        "kmeans_iterations": labeling.iterations_run, "solver_iterations": its.tolist(),
+        "solver_residuals": res.tolist(), "solver_converged": conv.tolist(), "ridge": icfg.ridge,
+        "zero_feature_rows": zero_rows.tolist(), "assign_fallback_nodes": fallback.tolist(), "warnings": warnings,
+        "ranks": grp.world, "columns_per_rank": {"d": dcols.stop - dcols.start, "k": kcols.stop - kcols.start},
+        "timings": {"total": time.perf_counter() - t_run},
+    }
+    return ClusterResult(labels=labels, soft=X, diagnostics=diagnostics, num_clusters=prm.k)

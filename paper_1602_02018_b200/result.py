@@ -34,10 +34,12 @@ def _plain(v: Any) -> Any:
 class ClusterResult:
     """Hard partition, soft indicators (N x k) and run diagnostics."""
 
-    def __init__(self, labels: np.ndarray, soft: Any, diagnostics: dict[str, Any] | None = None):
+    def __init__(self, labels: np.ndarray, soft: Any, diagnostics: dict[str, Any] | None = None,
+                 num_clusters: int | None = None):
         self.labels = labels
         self._soft = soft
         self.diagnostics = {} if diagnostics is None else diagnostics
+        self._k = num_clusters  # set when ``soft`` holds only this rank's columns (column-sharded runs)
 
     @property
     def soft(self) -> np.ndarray:
@@ -57,7 +59,7 @@ class ClusterResult:
 
     @property
     def num_clusters(self) -> int:
-        return int(self._soft.shape[1])
+        return int(self._k if self._k is not None else self._soft.shape[1])
 
     def to_dict(self, *, include_timings: bool = False) -> dict[str, Any]:
         diag = {k: _plain(v) for k, v in self.diagnostics.items() if include_timings or k != "timings"}

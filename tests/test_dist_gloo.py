@@ -1,0 +1,150 @@
+"""Column-sharded exchange logic (dist.py) with world_size 2 over gloo on CPU.
+
+The per-rank compute is an oracle-based CPU backend (test-only); what is under
+test is the sharding, the collectives and the merge rules, against the
+single-process oracle."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import D_C1, c1_config
+from oracle import cpu_ref as O
+from paper_1602_02018_b200 import dist as D
+from paper_1602_02018_b200.filters import design_lowpass
+from paper_1602_02018_b200.pipeline import CscParams
+from paper_1602_02018_b200.sampling import CgInfo
+from paper_1602_02018_b200.sbm import sbm_edges
+
+
+class OracleBackend:
+    """CPU per-rank compute for the tests (the product uses dist.DeviceBackend)."""
+
+    def __init__(self, csr):
+        self.csr = csr
+
+    def count(self, filt, R):
+        if R.shape[1] == 0:
+            return 0.0
+        Y = O.apply_filter(filt.coeffs, self.csr, R)
+        return float(np.sum(Y * Y))
+
+    def filter_rowsq(self, filt, R):
+        Y = O.apply_filter(filt.coeffs, self.csr, R) if R.shape[1] else np.zeros_like(R)
+        return Y, np.sum(Y * Y, axis=1)
+
+    def normalize(self, Y, rowsq):
+        nrm = np.sqrt(rowsq)
+        zero = np.flatnonzero(nrm <= 1e-300)
+        safe = nrm.copy()
+        safe[zero] = 1.0
+        F = Y / safe[:, None]
+        F[zero] = 0.0
+        return F, zero
+
+    def gather(self, F, idx):
+        return F[idx]
+
+    def block_cg(self, cfg, sampling, reduced):
+        if reduced.shape[1] == 0:
+            return np.zeros((self.csr.num_nodes, 0)), CgInfo(np.zeros(0, np.int64), np.zeros(0), np.zeros(0, bool))
+        X, its, res, conv = O.interpolate_all(self.csr, cfg.highpass.coeffs, cfg.gamma, cfg.ridge, sampling.indices,
+                                              reduced, cfg.solver_tol, cfg.solver_max_iters)
+        return X, CgInfo(its, res, conv)
+
+    def row_best(self, soft, col0):
+        norms = np.linalg.norm(soft, axis=0)
+        q = np.where(norms > 0, soft / np.where(norms > 0, norms, 1.0), -np.inf) if soft.shape[1] else np.full(
+            (soft.shape[0], 1), -np.inf)
+        idx = q.argmax(axis=1)
+        return q[np.arange(q.shape[0]), idx], col0 + idx, np.any(soft != 0, axis=1), bool(np.any(norms > 0))
+
+
+def c1_csr():
+    src, dst, _ = sbm_edges(c1_config())
+    return O.sbm_csr(src, dst, 1000)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fn, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out[rank] = fn(D.Group.current())
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(fn, world=2):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), fn, out), nprocs=world, join=True)
+    return [out[r] for r in range(world)]
+
+
+def test_column_slice_partitions():
+    for ncols in (1, 2, 7, 28, 56, 100):
+        for world in (1, 2, 3, 4, 8):
+            parts = [D.column_slice(ncols, world, r) for r in range(world)]
+            cover = np.concatenate([np.arange(p.start, p.stop) for p in parts])
+            assert np.array_equal(cover, np.arange(ncols))
+            sizes = [p.stop - p.start for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_merge_argmax_tie_rule():
+    v = [np.array([0.5, 0.2, 0.7]), np.array([0.5, 0.9, 0.1])]
+    c = [np.array([3, 1, 0]), np.array([7, 6, 5])]
+    assert D.merge_argmax(v, c).tolist() == [3, 6, 0]
+
+
+def _features_and_count(grp):
+    csr = c1_csr()
+    be = OracleBackend(csr)
+    R = O.gaussian_signals(1000, D_C1, O.substream(0, "signals"))
+    cols = D.column_slice(D_C1, grp.world, grp.rank)
+    filt = design_lowpass(0.45, 30)
+    F, zero = D.sharded_features(be, filt, np.ascontiguousarray(R[:, cols]), grp)
+    cnt = D.sharded_count(be, filt, np.ascontiguousarray(R[:, cols]), grp)
+    return cols.start, cols.stop, F, zero, cnt
+
+
+def test_sharded_features_and_count_match_single_process():
+    parts = run_world(_features_and_count)
+    csr = c1_csr()
+    R = O.gaussian_signals(1000, D_C1, O.substream(0, "signals"))
+    filt = design_lowpass(0.45, 30)
+    rows, zero = O.build_features(filt.coeffs, csr, R)
+    F = np.zeros_like(rows)
+    for c0, c1, Fl, z, cnt in parts:
+        F[:, c0:c1] = Fl
+        assert np.array_equal(z, zero)
+        ref = float(np.sum(O.apply_filter(filt.coeffs, csr, R) ** 2))
+        assert abs(cnt - ref) <= 1e-12 * ref
+    assert np.abs(F - rows).max() <= 1e-13
+
+
+def _run_sharded(grp):
+    be = OracleBackend(c1_csr())
+    res = D.run_csc_sharded(be, 1000, CscParams(k=20, d=D_C1, seed=0), grp)
+    return res.labels, res.diagnostics["lambda_k_hat"], res.diagnostics["solver_iterations"], res.num_clusters
+
+
+def test_run_csc_sharded_matches_reference(c1_golden):
+    parts = run_world(_run_sharded)
+    for labels, lam, its, k in parts:
+        assert lam == float(c1_golden["lambda_k_hat"])
+        assert its == c1_golden["solver_iterations"].tolist()
+        assert np.array_equal(labels, c1_golden["labels"])
+        assert k == 20

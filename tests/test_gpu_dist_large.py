@@ -1,0 +1,92 @@
+"""Device backend of the column-sharded path, and full-size (BASELINE config 3) properties."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import D_C1, relerr, sbm_config
+from gpu_util import c1_op, options
+from oracle import cpu_ref as O
+import paper_1602_02018_b200 as P
+from paper_1602_02018_b200 import dist as D
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_backend_single_rank_matches_reference(c1_golden):
+    grp = D.Group(0, 1)
+    res = D.run_csc_sharded(D.DeviceBackend(c1_op()), 1000, P.CscParams(k=20, d=D_C1, seed=0), grp)
+    assert res.diagnostics["lambda_k_hat"] == float(c1_golden["lambda_k_hat"])
+    assert res.diagnostics["solver_iterations"] == c1_golden["solver_iterations"].tolist()
+    assert np.array_equal(res.labels, c1_golden["labels"])
+
+
+def test_device_backend_partial_assign_matches_oracle():
+    import torch
+
+    rng = np.random.default_rng(7)
+    soft = rng.standard_normal((3000, 23))
+    soft[5] = 0.0
+    be = D.DeviceBackend(c1_op())
+    val, col, nz, any_norm = be.row_best(torch.tensor(soft[:, 10:], device="cuda"), 10)
+    q = soft[:, 10:] / np.linalg.norm(soft[:, 10:], axis=0)
+    assert np.array_equal(col, 10 + q.argmax(axis=1))
+    assert np.allclose(val, q.max(axis=1), rtol=0, atol=0)
+    assert not nz[5] and nz.sum() == 2999 and any_norm
+
+
+_big: dict = {}
+
+
+def c3_graph():
+    if "g" not in _big:
+        _big["g"] = P.sbm_generate(sbm_config(1_000_000, 100))
+    return _big["g"]
+
+
+def test_c3_graph_build_matches_scipy_path():
+    g, _ = c3_graph()
+    src, dst, _ = P.sbm.sbm_edges(sbm_config(1_000_000, 100))
+    ref = O.sbm_csr(src, dst, 1_000_000)
+    assert O.csr_digest(O.Csr(g.num_nodes, g.indptr, g.indices, g.weights, g.degrees)) == O.csr_digest(ref)
+
+
+def test_c3_fp32_vs_fp64_and_low_order_oracle():
+    """Full size: fp32 mode within 1e-4 of fp64; fp64 within 1e-12 of the oracle on a short filter."""
+    g, _ = c3_graph()
+    d = int(math.ceil(4 * math.log(1e6)))
+    X = np.random.default_rng(3).standard_normal((1_000_000, d)) / np.sqrt(d)
+    filt = P.design_lowpass(0.43, 50)
+    y64 = P.apply_filter(filt, P.laplacian_op(g), X)
+    y32 = P.apply_filter(filt, P.laplacian_op(g, dtype="float32"), X)
+    assert relerr(y32, y64) <= 1e-4
+    short = P.design_lowpass(0.43, 3)
+    csr = O.Csr(g.num_nodes, g.indptr, g.indices, g.weights, g.degrees)
+    assert relerr(P.apply_filter(short, P.laplacian_op(g), X[:, :4]), O.apply_filter(short.coeffs, csr, X[:, :4])) <= 1e-12
+
+
+def test_c3_size_independent_properties():
+    """Complementarity (low + high = I), linearity and symmetry at N = 1e6, both recurrences."""
+    g, _ = c3_graph()
+    op = P.laplacian_op(g)
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((1_000_000, 6))
+    Z = rng.standard_normal((1_000_000, 6))
+    low = P.design_lowpass(0.43, 50)
+    high = P.matched_highpass(low)
+    for rec in (0, 1):
+        with options(recurrence=rec):
+            lx = P.apply_filter(low, op, X)
+            assert np.abs(lx + P.apply_filter(high, op, X) - X).max() < 1e-11
+            lz = P.apply_filter(low, op, Z)
+            assert relerr(P.apply_filter(low, op, 2 * X - 3 * Z), 2 * lx - 3 * lz) < 1e-12
+            assert abs(np.sum(lx * Z) - np.sum(X * lz)) < 1e-9 * np.sqrt(np.sum(lx**2) * np.sum(Z**2))
+
+
+def test_c3_eigencount_full_spectrum():
+    g, _ = c3_graph()
+    est = P.eigencount(P.laplacian_op(g, dtype="float32"), 2.0, rng=np.random.default_rng(0))
+    assert abs(est.count - 1_000_000) <= 0.02 * 1_000_000
