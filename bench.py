@@ -317,6 +317,13 @@ def run_ours(args, cfg):
         "algorithmic_bytes_per_launch": step_bytes / max(step_launches, 1),
         "kernel_share_of_step": (step_ms / args.steps) / ms if ms > 0 else None,
         "recurrence": "clenshaw" if _lib.get_option("recurrence") == 0 else "forward",
+        # K2 is bound by the neighbour-gather traffic through L2 (deg x row bytes per step), not by
+        # DRAM: the gathered panel is L2-resident.  Measured ceiling for random 64-byte row gathers
+        # on this GPU: tools/microbench/gather_bench.cu (LDG, 64 warps/SM).
+        "l2_path": {"gather_bytes_per_launch": float(nnz) * 16 * 4,
+                    "achieved_gbs": (float(nnz) * 64 + step_bytes / max(step_launches, 1))
+                    / (step_ms / max(step_launches, 1) / 1e3) / 1e9 if step_ms > 0 else None,
+                    "ceiling_gbs": 11050.0, "ceiling_source": "tools/microbench/gather_bench.cu, profiles/r01_notes.md"},
     }
     cpub = None
     if world == 1 and not args.no_cpu:

@@ -86,8 +86,8 @@ struct Pair<double> {
   using type = double2;
 };
 
-template <typename T, int LPR, int EPI, int CHUNK, bool UNIT>
-__global__ void __launch_bounds__(256, (CHUNK <= 4 ? 4 : 2)) k_cheb_step(const StepArgs a) {
+template <typename T, int LPR, int EPI, int CHUNK, int MINB, bool UNIT>
+__global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
   using VT = Vec16<T>;
   using V = typename VT::type;
   using V2 = typename Pair<T>::type;
@@ -158,17 +158,10 @@ __global__ void __launch_bounds__(256, (CHUNK <= 4 ? 4 : 2)) k_cheb_step(const S
     const int cnt = nend - nbeg;
     const size_t off = (size_t)row * PW + col0;
 
-    // 1. row-local operands
+    // 1. row-local operands: loaded after the neighbour loop (latency hidden by
+    //    the other resident warps; keeping them live across it costs occupancy)
     T sv[VEC], xv[VEC], yv[VEC];
     V2 sc = {T(0), T(0)};
-#pragma unroll
-    for (int c = 0; c < VEC; ++c) sv[c] = xv[c] = yv[c] = T(0);
-    if (on) {
-      sc = rs[row];
-      if (S != nullptr) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(S + off)), sv);
-      if (want_x) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(X + off)), xv);
-      if (a.fwd) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(Yin + off)), yv);
-    }
 
     // 2. neighbour chunks: CH neighbours per chunk (the row's lanes hold UC
     //    indices each), next chunk's indices loaded before this chunk's gathers
@@ -242,6 +235,14 @@ __global__ void __launch_bounds__(256, (CHUNK <= 4 ? 4 : 2)) k_cheb_step(const S
 
     // 4. epilogue
     double rsq = 0.0;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) sv[c] = xv[c] = yv[c] = T(0);
+    if (on) {
+      sc = rs[row];
+      if (S != nullptr) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(S + off)), sv);
+      if (want_x) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(X + off)), xv);
+      if (a.fwd) VT::unpack(ld_stream(HINTS, reinterpret_cast<const V*>(Yin + off)), yv);
+    }
     if (on) {
       const T si = sc.x, sdi = sc.y;
       const bool isolated = si == T(0);
@@ -333,9 +334,9 @@ __global__ void __launch_bounds__(256, (CHUNK <= 4 ? 4 : 2)) k_cheb_step(const S
 
 // ---------------------------------------------------------------------------
 // dispatch
-template <typename T, int LPR, int EPI, int CHUNK, bool UNIT>
+template <typename T, int LPR, int EPI, int CHUNK, int MINB, bool UNIT>
 static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t s) {
-  auto kern = k_cheb_step<T, LPR, EPI, CHUNK, UNIT>;
+  auto kern = k_cheb_step<T, LPR, EPI, CHUNK, MINB, UNIT>;
   static std::mutex mu;
   static int occ_cache[64] = {0};  // per device
   int occ;
@@ -379,15 +380,15 @@ static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t
   return grid;
 }
 
-template <typename T, int EPI, int CHUNK, bool UNIT>
+template <typename T, int EPI, int CHUNK, int MINB, bool UNIT>
 static int launch_lpr(const StepArgs& a, int lpr, int threads, int device, cudaStream_t s) {
   switch (lpr) {
-    case 1: return launch_typed<T, 1, EPI, CHUNK, UNIT>(a, threads, device, s);
-    case 2: return launch_typed<T, 2, EPI, CHUNK, UNIT>(a, threads, device, s);
-    case 4: return launch_typed<T, 4, EPI, CHUNK, UNIT>(a, threads, device, s);
-    case 8: return launch_typed<T, 8, EPI, CHUNK, UNIT>(a, threads, device, s);
-    case 16: return launch_typed<T, 16, EPI, CHUNK, UNIT>(a, threads, device, s);
-    case 32: return launch_typed<T, 32, EPI, CHUNK, UNIT>(a, threads, device, s);
+    case 1: return launch_typed<T, 1, EPI, CHUNK, MINB, UNIT>(a, threads, device, s);
+    case 2: return launch_typed<T, 2, EPI, CHUNK, MINB, UNIT>(a, threads, device, s);
+    case 4: return launch_typed<T, 4, EPI, CHUNK, MINB, UNIT>(a, threads, device, s);
+    case 8: return launch_typed<T, 8, EPI, CHUNK, MINB, UNIT>(a, threads, device, s);
+    case 16: return launch_typed<T, 16, EPI, CHUNK, MINB, UNIT>(a, threads, device, s);
+    case 32: return launch_typed<T, 32, EPI, CHUNK, MINB, UNIT>(a, threads, device, s);
   }
   fail(CSC_ERR_INVALID, "unsupported panel width");
 }
@@ -395,14 +396,20 @@ static int launch_lpr(const StepArgs& a, int lpr, int threads, int device, cudaS
 template <typename T, int EPI>
 static int launch_epi(const StepArgs& a, int lpr, int threads, int device, cudaStream_t s) {
   // UNIT: unit-weight graph, no per-edge values are read
-  const bool chunk4 = g_opt.unroll.load() == 4;
+  // unroll: 8 -> 8 gathers in flight (2 CTAs/SM); 4 -> 4 in flight at 6 CTAs/SM (40 regs);
+  // 2 -> 4 in flight at 8 CTAs/SM (32 regs, full occupancy)
+  const int64_t mode = g_opt.unroll.load();
   const bool unit = a.wv == nullptr;
-  if (chunk4) {
-    if (unit) return launch_lpr<T, EPI, 4, true>(a, lpr, threads, device, s);
-    return launch_lpr<T, EPI, 4, false>(a, lpr, threads, device, s);
+  if (mode == 8) {
+    if (unit) return launch_lpr<T, EPI, 8, 2, true>(a, lpr, threads, device, s);
+    return launch_lpr<T, EPI, 8, 2, false>(a, lpr, threads, device, s);
   }
-  if (unit) return launch_lpr<T, EPI, 8, true>(a, lpr, threads, device, s);
-  return launch_lpr<T, EPI, 8, false>(a, lpr, threads, device, s);
+  if (mode == 2) {
+    if (unit) return launch_lpr<T, EPI, 4, 8, true>(a, lpr, threads, device, s);
+    return launch_lpr<T, EPI, 4, 8, false>(a, lpr, threads, device, s);
+  }
+  if (unit) return launch_lpr<T, EPI, 4, 6, true>(a, lpr, threads, device, s);
+  return launch_lpr<T, EPI, 4, 6, false>(a, lpr, threads, device, s);
 }
 
 int step_grid_cap(int device) {

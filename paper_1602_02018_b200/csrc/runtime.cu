@@ -166,7 +166,7 @@ int csc_set_option(const char* key, int64_t value) {
     if (k == "block_threads" && (value < 64 || value > 256 || value % 32))
       fail(CSC_ERR_INVALID, "block_threads must be a multiple of 32 in [64, 256]");
     if (k == "panel_width" && value < 0) fail(CSC_ERR_INVALID, "panel_width must be >= 0");
-    if (k == "unroll" && value != 4 && value != 8) fail(CSC_ERR_INVALID, "unroll must be 4 or 8");
+    if (k == "unroll" && value != 2 && value != 4 && value != 8) fail(CSC_ERR_INVALID, "unroll must be 2, 4 or 8");
     if (k == "l2_persist_pct" && (value < 0 || value > 100)) fail(CSC_ERR_INVALID, "l2_persist_pct in [0, 100]");
     if (k == "l2_budget_pct" && (value < 1 || value > 100)) fail(CSC_ERR_INVALID, "l2_budget_pct in [1, 100]");
     slot->store(value);
