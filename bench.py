@@ -320,10 +320,14 @@ def run_ours(args, cfg):
         # K2 is bound by the neighbour-gather traffic through L2 (deg x row bytes per step), not by
         # DRAM: the gathered panel is L2-resident.  Measured ceiling for random 64-byte row gathers
         # on this GPU: tools/microbench/gather_bench.cu (LDG, 64 warps/SM).
-        "l2_path": {"gather_bytes_per_launch": float(nnz) * 16 * 4,
-                    "achieved_gbs": (float(nnz) * 64 + step_bytes / max(step_launches, 1))
-                    / (step_ms / max(step_launches, 1) / 1e3) / 1e9 if step_ms > 0 else None,
-                    "ceiling_gbs": 11050.0, "ceiling_source": "tools/microbench/gather_bench.cu, profiles/r01_notes.md"},
+        "l2_path": {
+            "bytes_per_filter": (step_bytes / args.steps + P_ORDER * (nnz - N) * d * (4 if cfg["dtype"] == "float32" else 8)),
+            "achieved_gbs": ((step_bytes / args.steps + P_ORDER * (nnz - N) * d * (4 if cfg["dtype"] == "float32" else 8))
+                             / (step_ms / args.steps / 1e3) / 1e9) if step_ms > 0 else None,
+            "ceiling_gbs": 11050.0,
+            "ceiling_source": "random 64-B row gathers, LDG at 64 warps/SM: tools/microbench/gather_bench.cu",
+            "note": "L2->SM bytes = algorithmic bytes + (deg-1) extra reads of every gathered row per step",
+        },
     }
     cpub = None
     if world == 1 and not args.no_cpu:
