@@ -165,6 +165,16 @@ int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int ncoeffs, doubl
 int csc_assign(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dtype, int64_t* labels,
                uint8_t* fallback, int64_t* num_fallback, int device, void* stream);
 
+/* One k-means replicate from given initial centroids: Lloyd iterations with
+ * first-minimum labels, mean updates, farthest-point repair of empty clusters and
+ * the relative-inertia stop (kmeans.py:64-93).  points n x d and init k x d are
+ * row-major fp64 (host or device); labels_out int64[n], centroids_out k x d (may
+ * be NULL), *inertia_out / *iters_out as the reference's Labeling fields.  The
+ * k-means++ seeding stays on the host (numpy RNG, kmeans.py:46-61). */
+int csc_kmeans_lloyd(const double* points, int64_t n, int d, const double* init, int k, int64_t max_iters,
+                     double tol, int64_t* labels_out, double* centroids_out, double* inertia_out, int64_t* iters_out,
+                     int device, void* stream);
+
 /* Column-sharded assign: for this rank's columns [col_offset, col_offset + k) of
  * the soft indicators, per row the best normalised value (fp64, -inf if every
  * local column has zero norm), its global column (int64) and whether any local

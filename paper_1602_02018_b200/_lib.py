@@ -53,6 +53,7 @@ SIGNATURES: dict[str, list] = {
     "csc_block_cg": [_p, _p, _i32, _f64, _f64, _p, _i64, _p, _i32, _f64, _i64, _p, _i64, _i32,
                      _p, _p, _p, _p, _p],
     "csc_assign": [_p, _i64, _i64, _i32, _i32, _p, _p, _p, _i32, _p],
+    "csc_kmeans_lloyd": [_p, _i64, _i32, _p, _i32, _i64, _f64, _p, _p, _p, _p, _i32, _p],
     "csc_assign_partial": [_p, _i64, _i64, _i32, _i32, _i64, _p, _p, _p, _p, _i32, _p],
 }
 

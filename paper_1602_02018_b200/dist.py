@@ -185,6 +185,9 @@ class DeviceBackend:
             return X, CgInfo(np.zeros(0, np.int64), np.zeros(0), np.zeros(0, bool))
         return X, block_cg_into(self.op, cfg, sampling, reduced, X)
 
+    def kmeans(self, points: np.ndarray, cfg):
+        return kmeans(points, cfg, device=self.op.device)
+
     def row_best(self, soft, col0: int):
         N, k = int(soft.shape[0]), int(soft.shape[1])
         val = np.full(N, -np.inf)
@@ -288,7 +291,7 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
         warnings.append(f"{zero_rows.size} zero-norm feature rows")
     sampling = draw_sampling(N, prm.n, substream(prm.seed, "sampling"), exclude=zero_rows)
     rows = np.concatenate(grp.all_gather(backend.gather(F, sampling.indices)), axis=1)
-    labeling = kmeans(rows, prm.kmeans)
+    labeling = backend.kmeans(rows, prm.kmeans)
     counts = np.bincount(labeling.labels, minlength=prm.k)
     if np.any(counts == 0):
         from .pipeline import DegenerateClusteringError

@@ -58,6 +58,12 @@ class OracleBackend:
                                               reduced, cfg.solver_tol, cfg.solver_max_iters)
         return X, CgInfo(its, res, conv)
 
+    def kmeans(self, points, cfg):
+        from paper_1602_02018_b200.kmeans import Labeling
+
+        lab, inert, its = O.kmeans(points, cfg.k, cfg.seed, cfg.replicates, cfg.max_iters, cfg.tol)
+        return Labeling(lab, inert, its)
+
     def row_best(self, soft, col0):
         norms = np.linalg.norm(soft, axis=0)
         q = np.where(norms > 0, soft / np.where(norms > 0, norms, 1.0), -np.inf) if soft.shape[1] else np.full(

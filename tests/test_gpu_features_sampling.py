@@ -152,3 +152,27 @@ def test_gather_rows(c1_golden):
     F = torch.tensor(c1_golden["features"], device="cuda")
     rows = _gather_rows(F, c1_golden["indices"], 0)
     assert np.array_equal(rows, c1_golden["features"][c1_golden["indices"]])
+
+
+def test_kmeans_matches_golden(c1_golden):
+    from paper_1602_02018_b200._rng import substream_seed
+
+    rows = c1_golden["features"][c1_golden["indices"]]
+    lab = P.kmeans(rows, P.KmeansConfig(k=20, seed=substream_seed(0, "kmeans")))
+    assert np.array_equal(lab.labels, c1_golden["kmeans_labels"])
+    assert abs(lab.inertia - float(c1_golden["kmeans_inertia"])) <= 1e-12 * float(c1_golden["kmeans_inertia"])
+
+
+def test_kmeans_matches_oracle_random():
+    rng = np.random.default_rng(3)
+    for k, seed in ((6, 11), (9, 5)):
+        pts = np.concatenate([rng.normal(c, 0.35, (40, 5)) for c in range(6)])
+        a = P.kmeans(pts, P.KmeansConfig(k=k, seed=seed, replicates=5))
+        b = O.kmeans(pts, k, seed, replicates=5)
+        assert np.array_equal(a.labels, b[0]) and a.iterations_run == b[2]
+        assert abs(a.inertia - b[1]) <= 1e-12 * b[1]
+    # empty-cluster repair path: more clusters than distinct points
+    pts = np.repeat(np.eye(3), 4, axis=0)
+    a = P.kmeans(pts, P.KmeansConfig(k=5, seed=1, replicates=2))
+    b = O.kmeans(pts, 5, 1, replicates=2)
+    assert np.array_equal(a.labels, b[0]) and a.iterations_run == b[2]

