@@ -36,7 +36,18 @@ CONFIGS = {
     "c3": dict(N=1_000_000, k=100, s=16.0, dtype="float32", label="BASELINE config 3"),
     "c2": dict(N=100_000, k=20, s=16.0, dtype="float32", label="BASELINE config 2"),
     "c1": dict(N=1_000, k=20, s=16.0, dtype="float64", label="BASELINE config 1"),
+    "c4": dict(N=334_863, k=250, s=5.5, dtype="float32", label="BASELINE config 4 (DC-SBM, Pareto 2.5)", dcsbm=True),
 }
+
+
+def make_graph(P, cfg, device=None):
+    """The config's synthetic graph (seed 0) and ground truth."""
+    scfg = P.SbmConfig(num_nodes=cfg["N"], k=cfg["k"], avg_degree=cfg["s"],
+                       epsilon=P.critical_epsilon(cfg["s"], cfg["k"]) / 4.0, seed=0)
+    if cfg.get("dcsbm"):
+        g, truth, _ = P.dcsbm_generate(scfg, device=device)
+        return g, truth
+    return P.sbm_generate(scfg, device=device)
 P_ORDER = 50
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (GB/s)
 
@@ -106,7 +117,7 @@ class ClockSampler:
 
 def workload_config(cfg, N, nnz, d, world, extra=None):
     out = {
-        "workload": f"{cfg['label']}: SBM N={N}, k={cfg['k']}, s={cfg['s']:g}, eps=eps_c/4, seed 0; "
+        "workload": f"{cfg['label']}: {'DC-SBM' if cfg.get('dcsbm') else 'SBM'} N={N}, k={cfg['k']}, s={cfg['s']:g}, eps=eps_c/4, seed 0; "
                     f"features filter, d={d} N(0,1/d) signals per rank, Jackson-Chebyshev order {P_ORDER}",
         "N": N, "nnz": nnz, "d": d, "p": P_ORDER, "k": cfg["k"],
         "cache": "inputs larger than L2 (N x d fp32 block > 126 MB L2 at N=1e6); no flush",
@@ -134,7 +145,12 @@ def run_reference(args, cfg):
     N, k, s = cfg["N"], cfg["k"], cfg["s"]
     d = int(math.ceil(4 * math.log(N)))
     scfg = SbmConfig(num_nodes=N, k=k, avg_degree=s, epsilon=critical_epsilon(s, k) / 4.0, seed=0)
-    src, dst, _ = sbm_edges(scfg)
+    if cfg.get("dcsbm"):
+        from paper_1602_02018_b200.sbm import dcsbm_edges
+
+        src, dst, _, _ = dcsbm_edges(scfg)
+    else:
+        src, dst, _ = sbm_edges(scfg)
     g = O.sbm_csr(src, dst, N)
     nnz = int(g.indices.size)
     X = np.random.default_rng(0).standard_normal((N, d)) / np.sqrt(d)
@@ -202,8 +218,7 @@ def run_ours(args, cfg):
     grp = Group.current()  # column shards: each rank owns d signal columns of a (d x world)-column job
     N, k, s = cfg["N"], cfg["k"], cfg["s"]
     d = int(math.ceil(4 * math.log(N)))
-    scfg = P.SbmConfig(num_nodes=N, k=k, avg_degree=s, epsilon=P.critical_epsilon(s, k) / 4.0, seed=0)
-    graph, truth = P.sbm_generate(scfg, device=local)
+    graph, truth = make_graph(P, cfg, device=local)
     nnz = int(graph.indices.size)
     op = P.laplacian_op(graph, dtype=cfg["dtype"], device=local)
 

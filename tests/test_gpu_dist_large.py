@@ -90,3 +90,35 @@ def test_c3_eigencount_full_spectrum():
     g, _ = c3_graph()
     est = P.eigencount(P.laplacian_op(g, dtype="float32"), 2.0, rng=np.random.default_rng(0))
     assert abs(est.count - 1_000_000) <= 0.02 * 1_000_000
+
+
+def test_dcsbm_heavy_rows_parity():
+    """Degree-corrected SBM (BASELINE config 4 shape, smaller N): heavy-tailed rows vs the oracle."""
+    cfg = P.SbmConfig(num_nodes=40_000, k=40, avg_degree=5.5, epsilon=P.critical_epsilon(5.5, 40) / 4.0, seed=0)
+    g, truth, _ = P.dcsbm_generate(cfg)
+    deg = np.diff(g.indptr)
+    assert deg.max() > 15 * deg.mean()
+    csr = O.Csr(g.num_nodes, g.indptr, g.indices, g.weights, g.degrees)
+    src, dst, _, _ = P.sbm.dcsbm_edges(cfg)
+    assert O.csr_digest(csr) == O.csr_digest(O.sbm_csr(src, dst, cfg.num_nodes))
+    X = np.random.default_rng(1).standard_normal((cfg.num_nodes, 19))
+    filt = P.design_lowpass(0.3, 50)
+    ref = O.apply_filter(filt.coeffs, csr, X)
+    assert relerr(P.apply_filter(filt, P.laplacian_op(g), X), ref) <= 1e-12
+    assert relerr(P.apply_filter(filt, P.laplacian_op(g, dtype="float32"), X), ref) <= 1e-4
+    iso = g.isolated_nodes
+    y = P.apply_filter(filt, P.laplacian_op(g), X)
+    if iso.size:  # isolated nodes: h(1) X
+        assert np.allclose(y[iso], filt.evaluate(1.0) * X[iso], rtol=1e-12, atol=1e-14)
+
+
+def test_dcsbm_run_csc_vs_oracle():
+    cfg = P.SbmConfig(num_nodes=20_000, k=20, avg_degree=5.5, epsilon=P.critical_epsilon(5.5, 20) / 4.0, seed=0)
+    g, truth, _ = P.dcsbm_generate(cfg)
+    csr = O.Csr(g.num_nodes, g.indptr, g.indices, g.weights, g.degrees)
+    d = int(math.ceil(4 * math.log(cfg.num_nodes)))
+    r = P.run_csc(P.laplacian_op(g), P.CscParams(k=20, d=d, seed=0))
+    o = O.run_csc(csr, 20, d=d, seed=0)
+    assert r.diagnostics["lambda_k_hat"] == o["lambda_k_hat"]
+    assert r.diagnostics["zero_feature_rows"] == o["zero_rows"].tolist()
+    assert P.adjusted_rand_index(r.labels, o["labels"]) >= 0.99

@@ -15,7 +15,7 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
-from bench import CONFIGS, P_ORDER, filter_bytes  # noqa: E402
+from bench import CONFIGS, P_ORDER, filter_bytes, make_graph  # noqa: E402
 
 
 def main():
@@ -36,7 +36,7 @@ def main():
     dtype = args.dtype or cfg["dtype"]
     N, k, s = cfg["N"], cfg["k"], cfg["s"]
     d = args.width or int(math.ceil(4 * math.log(N)))
-    g, _ = P.sbm_generate(P.SbmConfig(num_nodes=N, k=k, avg_degree=s, epsilon=P.critical_epsilon(s, k) / 4, seed=0))
+    g, _ = make_graph(P, cfg)
     op = P.laplacian_op(g, dtype=dtype)
     tdt = torch.float32 if dtype == "float32" else torch.float64
     X = torch.randn(N, d, dtype=torch.float64, device="cuda").div_(math.sqrt(d)).to(tdt)
