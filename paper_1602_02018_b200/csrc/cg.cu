@@ -285,7 +285,7 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
     ensure_pool(g->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t N = g->n;
-    const PanelPlan pp = plan_panels(N, k, g->dtype, g->device);
+    const PanelPlan pp = plan_panels(N, k, g->dtype, g->device, g->nnz);
     const size_t cs = dtype_size(g->dtype);
 
     DeviceView didx(sample_idx, sizeof(int64_t) * std::max<int64_t>(n, 1), g->device, s);

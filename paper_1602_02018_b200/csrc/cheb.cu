@@ -625,7 +625,7 @@ template int filter_panel<double>(const csc_graph*, const double*, int, const do
 
 // ---------------------------------------------------------------------------
 // panels
-PanelPlan plan_panels(int64_t n, int w, int dtype, int device) {
+PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
   const int vec = 16 / (int)dtype_size(dtype);
   const int max_lpr = 32;
   int max_pw = vec * max_lpr;
@@ -635,8 +635,13 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device) {
     while (pw < forced && pw < max_pw) pw *= 2;
     max_pw = pw;
   } else {
-    // widest power-of-two panel whose gather source fits the L2 budget
-    const double budget = (double)device_props(device).l2_bytes * (double)g_opt.l2_budget_pct.load() / 100.0;
+    // widest power-of-two panel whose gather source fits the L2 budget.  Low-degree
+    // graphs re-read each gathered row fewer times, so L2 misses cost less than the
+    // extra CSR pass of another panel: the budget grows as 16 / mean degree (<= 4x).
+    const double deg = n > 0 ? (double)nnz / (double)n : 16.0;
+    const double relax = std::min(4.0, std::max(1.0, 16.0 / std::max(deg, 1.0)));
+    const double budget =
+        relax * (double)device_props(device).l2_bytes * (double)g_opt.l2_budget_pct.load() / 100.0;
     int pw = vec;
     while (pw * 2 <= max_pw && (double)n * (pw * 2) * dtype_size(dtype) <= budget) pw *= 2;
     if ((double)n * pw * dtype_size(dtype) > budget) pw = max_pw;  // nothing fits: minimise CSR passes
@@ -907,7 +912,7 @@ struct PackedInput {
   PanelPlan pp;
   Scratch x, xs;
   PackedInput(const csc_graph* g, const void* src, int64_t ld, int ncols, int io, cudaStream_t s) {
-    pp = plan_panels(g->n, ncols, g->dtype, g->device);
+    pp = plan_panels(g->n, ncols, g->dtype, g->device, g->nnz);
     const size_t cs = dtype_size(g->dtype);
     StagedIn in;
     stage_in(src, ld, g->n, ncols, io, g->device, s, in);

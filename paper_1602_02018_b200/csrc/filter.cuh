@@ -80,7 +80,7 @@ struct PanelPlan {
   int max_pw = 0;
 };
 
-PanelPlan plan_panels(int64_t n, int w, int dtype, int device);
+PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz);
 
 // Upper bound of the step kernel's grid (for sizing epilogue partials).
 int step_grid_cap(int device);
