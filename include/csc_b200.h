@@ -52,6 +52,9 @@ extern "C" {
 #define CSC_SELF_LOOPS_DROP 1  /* build_graph(self_loops="drop"),  graph.py:119-120 */
 
 typedef struct csc_graph csc_graph;
+typedef struct csc_comm csc_comm; /* NCCL communicator for row-sharded operators */
+
+#define CSC_UNIQUE_ID_BYTES 128
 
 /* ---- library ------------------------------------------------------------ */
 int csc_abi_version(void);
@@ -183,6 +186,29 @@ int csc_kmeans_lloyd(const double* points, int64_t n, int d, const double* init,
 int csc_assign_partial(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dtype, int64_t col_offset,
                        double* best_val, int64_t* best_col, uint8_t* nonzero, int* any_norm, int device,
                        void* stream);
+
+/* ---- row-sharded operator (BASELINE config 5) ------------- */
+/* NCCL communicator: rank 0 creates the id, the caller distributes it (e.g. a
+ * torch.distributed broadcast), every rank creates its communicator. */
+int csc_comm_unique_id(uint8_t* out /* CSC_UNIQUE_ID_BYTES */);
+int csc_comm_create(const uint8_t* unique_id, int nranks, int rank, int device, csc_comm** out);
+int csc_comm_destroy(csc_comm* comm);
+
+/* This rank's rows [row_begin, row_begin + num_rows) of an N-node graph as a
+ * CSR with global column indices (indptr local, starting at 0).  Ranks own
+ * R = ceil(N / nranks) consecutive rows each (the last may own fewer). */
+int csc_graph_create_rows(int64_t num_nodes, int64_t row_begin, int64_t num_rows, int64_t nnz,
+                          const int32_t* indptr, const int32_t* indices, const double* weights, int dtype,
+                          int device, void* stream, csc_graph** out);
+
+/* Chebyshev filter on a row-sharded block (X, Y: this rank's rows, device
+ * buffers): every step is followed by an ncclAllGather of the step's rows into
+ * the full gather panel.  mode 0: Y = h(L) X;  mode 1: *out = sum of squares of
+ * this rank's rows of h(L) X (eigencount partial, spectrum.py:86; Y unused);
+ * mode 2: Y plus out[i] = row sums of squares (features.py:80; complete per row). */
+int csc_cheb_filter_rows(const csc_graph* g, csc_comm* comm, const double* coeffs, int ncoeffs, const void* X,
+                         int64_t ldx, void* Y, int64_t ldy, int ncols, int io_dtype, int mode, double* out,
+                         void* stream);
 
 #ifdef __cplusplus
 }

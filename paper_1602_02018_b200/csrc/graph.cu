@@ -86,7 +86,7 @@ __global__ void k_cast_weights(const double* __restrict__ w, int64_t nnz, T* __r
 
 // CSR sanity for user-supplied arrays: flags[0] bad indptr, flags[1] bad index.
 __global__ void k_check_csr(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t n,
-                            int64_t nnz, int* flags) {
+                            int64_t ncols, int64_t nnz, int* flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t b = indptr[i], e = indptr[i + 1];
     if (b < 0 || e < b || e > nnz) {
@@ -95,7 +95,7 @@ __global__ void k_check_csr(const int32_t* __restrict__ indptr, const int32_t* _
     }
     for (int32_t k = b; k < e; ++k) {
       const int32_t j = indices[k];
-      if (j < 0 || j >= n) atomicOr(&flags[1], 1);
+      if (j < 0 || j >= ncols) atomicOr(&flags[1], 1);
     }
   }
 }
@@ -193,6 +193,7 @@ csc_graph* graph_from_device_csr(int64_t n, int64_t nnz, int32_t* indptr, int32_
   g->indptr = indptr;
   g->indices = indices;
   g->weights = weights;
+  g->n_global = n;
   try {
     const size_t es = dtype_size(dtype);
     CSC_CUDA(cudaMalloc(&g->degrees, sizeof(double) * (n > 0 ? n : 1)));
@@ -266,17 +267,34 @@ static void check_common(int64_t num_nodes, int dtype, int device, csc_graph** o
   if (device < 0 || device >= ndev) fail(CSC_ERR_INVALID, "device " + std::to_string(device) + " not present");
 }
 
+namespace csc {
+// canonical CSR with num_nodes rows and column indices < ncols -> device operator
+csc_graph* graph_create_impl(int64_t num_nodes, int64_t ncols, int64_t nnz, const int32_t* indptr,
+                             const int32_t* indices, const double* weights, int dtype, int device, cudaStream_t s);
+}  // namespace csc
+
 extern "C" {
 
 int csc_graph_create(int64_t num_nodes, int64_t nnz, const int32_t* indptr, const int32_t* indices,
                      const double* weights, int dtype, int device, void* stream, csc_graph** out) {
   return guard([&] {
     check_common(num_nodes, dtype, device, out);
+    *out = graph_create_impl(num_nodes, num_nodes, nnz, indptr, indices, weights, dtype, device,
+                             static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"
+
+csc_graph* csc::graph_create_impl(int64_t num_nodes, int64_t ncols, int64_t nnz, const int32_t* indptr,
+                                  const int32_t* indices, const double* weights, int dtype, int device,
+                                  cudaStream_t s) {
+  csc_graph* result = nullptr;
+  {
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) fail(CSC_ERR_INVALID, "nnz out of int32 range");
     if (!indptr || (nnz > 0 && (!indices || !weights))) fail(CSC_ERR_INVALID, "CSR array is NULL");
     DeviceGuard dg(device);
     ensure_pool(device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t *d_ptr = nullptr, *d_idx = nullptr;
     double* d_w = nullptr;
     try {
@@ -294,7 +312,7 @@ int csc_graph_create(int64_t num_nodes, int64_t nnz, const int32_t* indptr, cons
       Scratch flags(2 * sizeof(int), s);
       CSC_CUDA(cudaMemsetAsync(flags.get(), 0, 2 * sizeof(int), s));
       if (num_nodes > 0) {
-        k_check_csr<<<grid_for(num_nodes), kThreads, 0, s>>>(d_ptr, d_idx, num_nodes, nnz, flags.as<int>());
+        k_check_csr<<<grid_for(num_nodes), kThreads, 0, s>>>(d_ptr, d_idx, num_nodes, ncols, nnz, flags.as<int>());
         CSC_LAUNCHED();
       }
       int hflags[2];
@@ -303,19 +321,21 @@ int csc_graph_create(int64_t num_nodes, int64_t nnz, const int32_t* indptr, cons
       if (ends[0] != 0 || ends[1] != nnz) fail(CSC_ERR_GRAPH, "indptr must start at 0 and end at nnz");
       if (hflags[0]) fail(CSC_ERR_GRAPH, "indptr is not non-decreasing");
       if (hflags[1]) fail(CSC_ERR_GRAPH, "column index out of range");
-      csc_graph* g = graph_from_device_csr(num_nodes, nnz, d_ptr, d_idx, d_w, dtype, device, s);
+      result = graph_from_device_csr(num_nodes, nnz, d_ptr, d_idx, d_w, dtype, device, s);
       d_ptr = nullptr;
       d_idx = nullptr;
       d_w = nullptr;
-      *out = g;
     } catch (...) {
       cudaFree(d_ptr);
       cudaFree(d_idx);
       cudaFree(d_w);
       throw;
     }
-  });
+  }
+  return result;
 }
+
+extern "C" {
 
 int csc_graph_build_coo(int64_t num_nodes, int64_t num_edges, const int64_t* src, const int64_t* dst,
                         const double* weights, int self_loops, int dtype, int device, void* stream,

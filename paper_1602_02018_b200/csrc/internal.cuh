@@ -233,6 +233,8 @@ struct csc_graph {
   double* degrees = nullptr;   // [n] row sums
   double* dis = nullptr;       // [n] d^-1/2 (0 where d == 0)
   bool unit = false;
+  int64_t n_global = 0;   // columns / global nodes (== n unless row-sharded)
+  int64_t row_begin = 0;  // first global row held (row-sharded operators)
 };
 
 namespace csc {

@@ -319,3 +319,109 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
         "timings": {"total": time.perf_counter() - t_run},
     }
     return ClusterResult(labels=labels, soft=X, diagnostics=diagnostics, num_clusters=prm.k)
+
+
+# ---------------------------------------------------------------------------
+# Row sharding (BASELINE config 5): the CSR is split by rows, the dense block
+# is all-gathered over NCCL after every Chebyshev step (inside the library).
+
+
+def row_range(num_nodes: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows owned by ``rank``: R = ceil(N / world) consecutive rows (the last rank may own fewer)."""
+    R = -(-num_nodes // world)
+    begin = min(num_nodes, rank * R)
+    return begin, min(num_nodes, begin + R)
+
+
+def local_csr(graph, begin: int, end: int):
+    """Rows [begin, end) of a canonical CSR, indptr rebased to 0, global column indices."""
+    lo, hi = int(graph.indptr[begin]), int(graph.indptr[end])
+    indptr = np.ascontiguousarray(graph.indptr[begin : end + 1] - lo, dtype=np.int32)
+    return indptr, np.ascontiguousarray(graph.indices[lo:hi], dtype=np.int32), np.ascontiguousarray(graph.weights[lo:hi])
+
+
+class RowShardedOperator:
+    """This rank's rows of the normalized Laplacian plus an NCCL communicator.
+
+    Blocks are passed as this rank's rows (CUDA tensors, N_local x w).
+    """
+
+    def __init__(self, graph, grp: Group, dtype: str = "float32", device: int | None = None):
+        import torch
+
+        self.grp = grp
+        self.num_nodes = graph.num_nodes
+        self.device = _lib.default_device() if device is None else int(device)
+        self.begin, self.end = row_range(graph.num_nodes, grp.world, grp.rank)
+        self.dtype = dtype
+        indptr, indices, weights = local_csr(graph, self.begin, self.end)
+        h = C.c_void_p()
+        _lib.call("csc_graph_create_rows", graph.num_nodes, self.begin, self.end - self.begin, int(indices.size),
+                  _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(weights), _lib.dtype_code(dtype), self.device,
+                  _lib.current_stream(self.device), C.byref(h))
+        self.handle = h.value
+        uid = np.zeros(128, dtype=np.uint8)
+        if grp.rank == 0:
+            _lib.call("csc_comm_unique_id", _lib.ptr(uid))
+        if grp.world > 1:
+            import torch.distributed as dist
+
+            t = torch.from_numpy(uid).to(grp.device)
+            dist.broadcast(t, src=0, group=grp.group)
+            uid = t.cpu().numpy()
+        comm = C.c_void_p()
+        _lib.call("csc_comm_create", _lib.ptr(uid), grp.world, grp.rank, self.device, C.byref(comm))
+        self.comm = comm.value
+
+    @property
+    def num_local(self) -> int:
+        return self.end - self.begin
+
+    def _run(self, filt: PolyFilter, X, mode: int):
+        import torch
+
+        c = coeff_array(filt)
+        Y = torch.empty_like(X) if mode != 1 else None
+        out = None
+        if mode == 1:
+            out = np.zeros(1)
+        elif mode == 2:
+            out = torch.empty(X.shape[0], dtype=torch.float64, device=X.device)
+        _lib.call("csc_cheb_filter_rows", self.handle, self.comm, _lib.ptr(c), int(c.size), X.data_ptr(),
+                  int(X.stride(0)), None if Y is None else Y.data_ptr(), int(X.shape[1]), int(X.shape[1]),
+                  _lib.dtype_code(X.dtype), mode, _lib.ptr(out), _lib.current_stream(self.device))
+        return Y, out
+
+    def apply_filter(self, filt: PolyFilter, X_local):
+        """h(L) X for this rank's rows."""
+        return self._run(filt, X_local.contiguous(), 0)[0]
+
+    def eigencount(self, filt: PolyFilter, R_local) -> float:
+        """sum((h(L) R)^2) over all ranks (partials summed in rank order)."""
+        _, part = self._run(filt, R_local.contiguous(), 1)
+        return float(self.grp.sum_in_order(part)[0])
+
+    def features(self, filt: PolyFilter, R_local):
+        """Row-normalised features of this rank's rows (rows are complete per rank: no exchange)."""
+        import torch
+
+        Y, rowsq = self._run(filt, R_local.contiguous(), 2)
+        F = torch.empty_like(Y)
+        flags = torch.zeros(Y.shape[0], dtype=torch.uint8, device=Y.device)
+        nz = C.c_int64(0)
+        _lib.call("csc_normalize_rows", Y.data_ptr(), int(Y.shape[1]), int(Y.shape[0]), int(Y.shape[1]),
+                  _lib.dtype_code(Y.dtype), rowsq.data_ptr(), F.data_ptr(), int(F.shape[1]), flags.data_ptr(),
+                  C.byref(nz), self.device, _lib.current_stream(self.device))
+        zero = flags.nonzero().flatten().cpu().numpy() + self.begin if nz.value else np.empty(0, dtype=np.int64)
+        return F, zero.astype(np.int64)
+
+    def __del__(self):
+        lib = _lib._lib
+        if lib is None:
+            return
+        if getattr(self, "comm", None):
+            lib.csc_comm_destroy(self.comm)
+            self.comm = None
+        if getattr(self, "handle", None):
+            lib.csc_graph_destroy(self.handle)
+            self.handle = None

@@ -154,3 +154,60 @@ def test_run_csc_sharded_matches_reference(c1_golden):
         assert its == c1_golden["solver_iterations"].tolist()
         assert np.array_equal(labels, c1_golden["labels"])
         assert k == 20
+
+
+# ---- row sharding (BASELINE config 5) -----------------------------------------
+
+
+def test_row_range_partitions():
+    for N in (1, 7, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            ranges = [D.row_range(N, world, r) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == N
+            for (a, b), (c, d) in zip(ranges, ranges[1:]):
+                assert b == c
+            assert max(b - a for a, b in ranges) == -(-N // world)
+
+
+def _row_sharded_filter(grp):
+    """The row-sharded recurrence of rows.cu, restated with numpy: local rows x full block,
+    block all-gathered after every step (equal R-row chunks, padded)."""
+    import scipy.sparse as sp
+
+    csr = c1_csr()
+    N = csr.num_nodes
+    b, e = D.row_range(N, grp.world, grp.rank)
+    R = -(-N // grp.world)
+    indptr, indices, weights = D.local_csr(csr, b, e)
+    Wl = sp.csr_matrix((weights, indices, indptr), shape=(e - b, N))
+    dis = csr.dis
+    X = O.gaussian_signals(N, 9, O.substream(0, "signals"))
+    c = design_lowpass(0.4, 30).coeffs
+
+    def gather(local):
+        pad = np.zeros((R, local.shape[1]))
+        pad[: local.shape[0]] = local
+        return np.concatenate(grp.all_gather(pad), axis=0)[:N]
+
+    def A(full, rows):  # (L - I) restricted to this rank's rows: -D^-1/2 W D^-1/2
+        return -(dis[b:e, None] * (Wl @ (dis[:, None] * full)))
+
+    Xl = X[b:e]
+    out = c[0] * Xl
+    t_prev, t_cur = Xl, A(X, Xl)
+    out = out + c[1] * t_cur
+    for l in range(2, c.size):
+        t_prev, t_cur = t_cur, 2.0 * A(gather(t_cur), t_cur) - t_prev
+        out = out + c[l] * t_cur
+    return b, e, out
+
+
+def test_row_sharded_recurrence_matches_oracle():
+    parts = run_world(_row_sharded_filter)
+    csr = c1_csr()
+    X = O.gaussian_signals(1000, 9, O.substream(0, "signals"))
+    ref = O.apply_filter(design_lowpass(0.4, 30).coeffs, csr, X)
+    got = np.zeros_like(ref)
+    for b, e, out in parts:
+        got[b:e] = out
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()

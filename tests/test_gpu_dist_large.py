@@ -122,3 +122,26 @@ def test_dcsbm_run_csc_vs_oracle():
     assert r.diagnostics["lambda_k_hat"] == o["lambda_k_hat"]
     assert r.diagnostics["zero_feature_rows"] == o["zero_rows"].tolist()
     assert P.adjusted_rand_index(r.labels, o["labels"]) >= 0.99
+
+
+def test_row_sharded_single_rank_matches_replicated():
+    """Row-sharded operator (NCCL all-gather after every step) with one rank == the replicated path."""
+    import torch
+
+    g = c1_op().graph
+    for dtype, tol in (("float64", 1e-12), ("float32", 1e-5)):
+        rop = D.RowShardedOperator(g, D.Group(0, 1), dtype=dtype)
+        op = P.laplacian_op(g, dtype=dtype)
+        X = np.random.default_rng(2).standard_normal((1000, 21))
+        filt = P.design_lowpass(0.45, 50)
+        tdt = torch.float64 if dtype == "float64" else torch.float32
+        Xt = torch.tensor(X, dtype=tdt, device="cuda")
+        y = rop.apply_filter(filt, Xt).double().cpu().numpy()
+        assert relerr(y, P.apply_filter(filt, op, X)) <= tol
+        cnt = rop.eigencount(filt, Xt)
+        ref = float(np.sum(P.apply_filter(filt, op, X) ** 2))
+        assert abs(cnt - ref) <= tol * ref
+        F, zero = rop.features(filt, Xt)
+        fref = P.build_features(op, filt, P.features.RandomSignals(X, "gaussian", None))
+        assert relerr(F.double().cpu().numpy(), fref.rows) <= tol
+        assert np.array_equal(zero, fref.zero_rows)
