@@ -187,6 +187,18 @@ int csc_assign_partial(const void* soft, int64_t ld, int64_t num_rows, int k, in
                        double* best_val, int64_t* best_col, uint8_t* nonzero, int* any_norm, int device,
                        void* stream);
 
+/* ---- parity RNG --------------------------------------------------------- */
+/* numpy's Generator(PCG64).standard_normal reproduced bit for bit on the device
+ * (the signal draws of spectrum.py:84 / features.py:63).  Tables: numpy's
+ * 256-layer ziggurat (ki uint64, wi, fi fp64), read from the installed numpy by
+ * the caller.  csc_numpy_normals writes `count` draws divided by `divisor` to
+ * out (fp64, host or device) starting from the 128-bit PCG64 state/increment,
+ * and returns in *raw_consumed how many 64-bit outputs the draws used (advance
+ * the numpy generator by that much to continue the stream). */
+int csc_set_normal_tables(const uint64_t* ki, const double* wi, const double* fi);
+int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                      double divisor, double* out, int64_t* raw_consumed, int device, void* stream);
+
 /* ---- row-sharded operator (BASELINE config 5) ------------- */
 /* NCCL communicator: rank 0 creates the id, the caller distributes it (e.g. a
  * torch.distributed broadcast), every rank creates its communicator. */

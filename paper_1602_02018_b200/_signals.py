@@ -72,3 +72,65 @@ class ProbeStream:
             self._next.result()
         finally:
             self._pool.shutdown(wait=True)
+
+
+# ---------------------------------------------------------------------------
+# device parity RNG (numpy's PCG64 + ziggurat reproduced bit for bit, csc_numpy_normals)
+
+_tables_loaded = False
+
+
+def device_rng_available() -> bool:
+    """True when numpy's ziggurat tables could be read and verified (see _npzig)."""
+    global _tables_loaded
+    if _tables_loaded:
+        return True
+    try:
+        from . import _lib
+        from ._npzig import ziggurat_tables
+
+        ki, wi, fi = ziggurat_tables()
+        _lib.call("csc_set_normal_tables", _lib.ptr(ki), _lib.ptr(wi), _lib.ptr(fi))
+        _tables_loaded = True
+    except Exception:
+        _tables_loaded = False
+    return _tables_loaded
+
+
+def device_normal_block(rng: np.random.Generator, n: int, w: int, device: int = 0, out=None):
+    """``rng.standard_normal((n, w)) / sqrt(w)`` drawn on the GPU into a CUDA fp64 tensor,
+    bit-identical to numpy; ``rng`` is advanced exactly as the host draw would advance it."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from ._npzig import pcg_state
+
+    if not device_rng_available():
+        raise RuntimeError("device parity RNG unavailable (numpy ziggurat tables not found)")
+    state, inc = pcg_state(rng)
+    if out is None:
+        out = torch.empty((n, w), dtype=torch.float64, device=f"cuda:{device}")
+    consumed = C.c_int64(0)
+    divisor = float(np.sqrt(w))
+    _lib.call("csc_numpy_normals", C.c_uint64(state >> 64), C.c_uint64(state & ((1 << 64) - 1)),
+              C.c_uint64(inc >> 64), C.c_uint64(inc & ((1 << 64) - 1)), int(n) * int(w), divisor, out.data_ptr(),
+              C.byref(consumed), int(device), _lib.current_stream(device))
+    rng.bit_generator.advance(int(consumed.value))
+    return out
+
+
+class DeviceProbeStream:
+    """Sequential probe blocks drawn on the GPU (same values as ProbeStream)."""
+
+    def __init__(self, rng: np.random.Generator, n: int, ds: int, device: int):
+        self.rng, self.n, self.ds, self.device = rng, n, ds, device
+        self.buf = None
+
+    def take(self):
+        self.buf = device_normal_block(self.rng, self.n, self.ds, self.device, self.buf)
+        return self.buf
+
+    def close(self) -> None:
+        pass

@@ -1,0 +1,352 @@
+// Parity RNG on the device: numpy's Generator(PCG64).standard_normal, bit-exact.
+//
+// The reference draws its probe and feature signals from seeded numpy streams
+// (spectrum.py:84, features.py:63); on the host that is ~90 M normals/s, the
+// dominant cost of run_csc at N = 1e6.  The stream is reproduced here:
+//   1. device: PCG64 raw outputs u_i (128-bit LCG jump-ahead per thread chunk,
+//      XSL-RR output); a raw is "special" if, as the start of a draw, it fails
+//      the ziggurat's fast test (rabs >= ki[layer]) -- ~1 % of positions;
+//   2. host: a sequential walk over the special positions decides which are
+//      draw starts and evaluates their wedge / tail paths with the C library's
+//      exp / log1p (the functions numpy's own C code calls), recording each
+//      start's value and how many raws it consumed;
+//   3. device: positions consumed inside slow paths are masked, a scan numbers
+//      the remaining starts, fast draws are +-rabs * wi[layer], and every value
+//      is divided by `divisor` into the output.
+// The caller advances its numpy generator by the returned raw count, so later
+// host draws continue the same stream.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <vector>
+
+#include "internal.cuh"
+
+using u128 = unsigned __int128;
+
+namespace csc {
+namespace {
+
+constexpr double kZigR = 3.6541528853610087963519472518;
+constexpr double kZigInvR = 0.27366123732975827203338247596;
+
+__constant__ uint64_t c_ki[256];
+__constant__ double c_wi[256];
+
+struct Tables {
+  uint64_t ki[256];
+  double wi[256];
+  double fi[256];
+  bool set = false;
+};
+Tables g_tab;
+std::mutex g_tab_mu;
+
+__host__ __device__ inline u128 make128(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
+
+__host__ __device__ inline u128 pcg_mult() { return make128(0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull); }
+
+// state after `delta` LCG steps
+__host__ __device__ inline u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
+  u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+// step then output (numpy's pcg64 next_uint64)
+__host__ __device__ inline uint64_t pcg_next(u128& state, u128 inc) {
+  state = state * pcg_mult() + inc;
+  const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+  const uint64_t x = hi ^ lo;
+  const unsigned r = (unsigned)(hi >> 58);
+  return (x >> r) | (x << ((64u - r) & 63u));
+}
+
+constexpr int kChunk = 64;  // raws per thread
+
+__global__ void k_pcg_raw(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, int64_t m,
+                          uint64_t* __restrict__ raw, uint8_t* __restrict__ special) {
+  const u128 inc = make128(i_hi, i_lo);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c * kChunk < m; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = c * kChunk;
+    u128 st = pcg_advance(make128(s_hi, s_lo), inc, (uint64_t)i0);
+    const int64_t i1 = min(m, i0 + kChunk);
+    for (int64_t i = i0; i < i1; ++i) {
+      const uint64_t u = pcg_next(st, inc);
+      raw[i] = u;
+      const unsigned idx = (unsigned)(u & 0xff);
+      const uint64_t rabs = ((u >> 8) >> 1) & 0x000fffffffffffffull;
+      special[i] = rabs >= c_ki[idx] ? 1 : 0;
+    }
+  }
+}
+
+// positions consumed inside slow paths are not draw starts
+__global__ void k_mark_skips(const int64_t* __restrict__ skip_begin, const int32_t* __restrict__ skip_len, int64_t nskip,
+                             int64_t m, uint32_t* __restrict__ is_start) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nskip; t += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < skip_len[t]; ++k) {
+      const int64_t p = skip_begin[t] + k;
+      if (p < m) is_start[p] = 0;
+    }
+}
+
+__global__ void k_gather_near(const uint64_t* __restrict__ raw, const int64_t* __restrict__ pos, int64_t nspec,
+                              int64_t m, int near, uint64_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nspec * near; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = t / near;
+    const int64_t p = pos[q] + (t - q * near);
+    out[t] = raw[p < m ? p : m - 1];
+  }
+}
+
+__global__ void k_init_starts(int64_t m, uint32_t* __restrict__ is_start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    is_start[i] = 1;
+}
+
+__global__ void k_emit(const uint64_t* __restrict__ raw, const uint8_t* __restrict__ special,
+                       const uint32_t* __restrict__ is_start, const uint32_t* __restrict__ index, int64_t m,
+                       int64_t count, const int64_t* __restrict__ sp_pos, const double* __restrict__ sp_val,
+                       int64_t nsp, double divisor, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!is_start[i]) continue;
+    const int64_t j = index[i];
+    if (j >= count) continue;
+    double v;
+    if (special[i]) {
+      int64_t lo = 0, hi = nsp;  // sp_pos sorted
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sp_pos[mid] < i)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      v = sp_val[lo];
+    } else {
+      const uint64_t u = raw[i];
+      const unsigned idx = (unsigned)(u & 0xff);
+      const uint64_t r = u >> 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+      v = (double)rabs * c_wi[idx];
+      if (r & 1) v = -v;
+    }
+    out[j] = v / divisor;
+  }
+}
+
+// Host evaluation of one draw starting at raw position `pos` (the slow path of
+// numpy's random_standard_normal); `raw` holds the device-generated stream,
+// positions beyond it are produced by jump-ahead.  Returns the value and sets
+// the number of raws consumed.
+struct HostStream {
+  const uint64_t* near;  // raws pos .. pos + nnear - 1
+  int64_t nnear;
+  int64_t pos;
+  u128 s0, inc;
+  int64_t k = 0;
+  uint64_t next() {
+    const int64_t i = k++;
+    if (i < nnear) return near[i];
+    u128 st = pcg_advance(s0, inc, (uint64_t)(pos + i));
+    return pcg_next(st, inc);
+  }
+  double next_double() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); }
+};
+
+double slow_draw(HostStream& hs, const Tables& t) {
+  for (;;) {
+    uint64_t r = hs.next();
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+    double x = (double)rabs * t.wi[idx];
+    if (sign) x = -x;
+    if (rabs < t.ki[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        const double xx = -kZigInvR * std::log1p(-hs.next_double());
+        const double yy = -std::log1p(-hs.next_double());
+        if (yy + yy > xx * xx) return ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
+      }
+    } else {
+      if ((t.fi[idx - 1] - t.fi[idx]) * hs.next_double() + t.fi[idx] < std::exp(-0.5 * x * x)) return x;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace csc
+
+using namespace csc;
+
+extern "C" {
+
+int csc_set_normal_tables(const uint64_t* ki, const double* wi, const double* fi) {
+  return guard([&] {
+    if (!ki || !wi || !fi) fail(CSC_ERR_INVALID, "NULL table");
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    std::memcpy(g_tab.ki, ki, sizeof(g_tab.ki));
+    std::memcpy(g_tab.wi, wi, sizeof(g_tab.wi));
+    std::memcpy(g_tab.fi, fi, sizeof(g_tab.fi));
+    g_tab.set = true;
+  });
+}
+
+int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                      double divisor, double* out, int64_t* raw_consumed, int device, void* stream) {
+  return guard([&] {
+    if (count < 0) fail(CSC_ERR_INVALID, "count must be >= 0");
+    if (!out && count > 0) fail(CSC_ERR_INVALID, "out is NULL");
+    if (!raw_consumed) fail(CSC_ERR_INVALID, "raw_consumed is NULL");
+    Tables t;
+    {
+      std::lock_guard<std::mutex> lk(g_tab_mu);
+      if (!g_tab.set) fail(CSC_ERR_INVALID, "normal tables not set (csc_set_normal_tables)");
+      t = g_tab;
+    }
+    if (count == 0) {
+      *raw_consumed = 0;
+      return;
+    }
+    DeviceGuard dg(device);
+    ensure_pool(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_ki, t.ki, sizeof(t.ki), 0, cudaMemcpyHostToDevice, s));
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_wi, t.wi, sizeof(t.wi), 0, cudaMemcpyHostToDevice, s));
+    const u128 s0 = make128(state_hi, state_lo), inc = make128(inc_hi, inc_lo);
+    DeviceOut dout(out, sizeof(double) * count, device, s);
+
+    int64_t m = count + count / 16 + 4096;  // ~2.2 % of raws are consumed inside slow paths
+    for (int attempt = 0; attempt < 4; ++attempt, m = m * 2) {
+      Scratch raw(sizeof(uint64_t) * m, s), special(m, s);
+      const int64_t chunks = (m + kChunk - 1) / kChunk;
+      k_pcg_raw<<<(int)std::min<int64_t>((chunks + 255) / 256, 65535), 256, 0, s>>>(
+          (uint64_t)(s0 >> 64), (uint64_t)s0, inc_hi, inc_lo, m, raw.as<uint64_t>(), special.as<uint8_t>());
+      CSC_LAUNCHED();
+      // compact the special positions (stable)
+      Scratch pos(sizeof(int64_t) * m, s), nsel(sizeof(int64_t), s);
+      size_t tb = 0;
+      thrust::counting_iterator<int64_t> it(0);
+      CSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, special.as<uint8_t>(), pos.as<int64_t>(),
+                                          nsel.as<int64_t>(), m, s));
+      Scratch tmp(tb, s);
+      CSC_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, special.as<uint8_t>(), pos.as<int64_t>(),
+                                          nsel.as<int64_t>(), m, s));
+      CSC_LAUNCHED();
+      int64_t nspec = 0;
+      CSC_CUDA(cudaMemcpyAsync(&nspec, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      CSC_CUDA(cudaStreamSynchronize(s));
+      std::vector<int64_t> hpos(nspec);
+      if (nspec) CSC_CUDA(cudaMemcpy(hpos.data(), pos.get(), sizeof(int64_t) * nspec, cudaMemcpyDeviceToHost));
+      // raws following each special position (slow paths read a few more)
+      constexpr int kNear = 8;
+      std::vector<uint64_t> hraw((size_t)nspec * kNear);
+      if (nspec) {
+        Scratch gath(sizeof(uint64_t) * nspec * kNear, s);
+        k_gather_near<<<(int)std::min<int64_t>((nspec * kNear + 255) / 256, 65535), 256, 0, s>>>(
+            raw.as<uint64_t>(), pos.as<int64_t>(), nspec, m, kNear, gath.as<uint64_t>());
+        CSC_LAUNCHED();
+        CSC_CUDA(cudaMemcpyAsync(hraw.data(), gath.get(), sizeof(uint64_t) * nspec * kNear, cudaMemcpyDeviceToHost, s));
+        CSC_CUDA(cudaStreamSynchronize(s));
+      }
+      // sequential walk: which specials start a draw, their values and consumption
+      std::vector<int64_t> sp_pos, skip_begin;
+      std::vector<double> sp_val;
+      std::vector<int32_t> skip_len;
+      int64_t next_free = 0, skipped = 0;
+      for (int64_t q = 0; q < nspec; ++q) {
+        const int64_t p = hpos[q];
+        if (p < next_free) continue;    // consumed by an earlier slow path
+        if (p - skipped >= count) break;  // draws before p already complete the request
+        HostStream hs{hraw.data() + q * kNear, std::min<int64_t>(kNear, m - p), p, s0, inc};
+        const double v = slow_draw(hs, t);
+        sp_pos.push_back(p);
+        sp_val.push_back(v);
+        if (hs.k > 1) {
+          skip_begin.push_back(p + 1);
+          skip_len.push_back((int32_t)(hs.k - 1));
+          skipped += hs.k - 1;
+        }
+        next_free = p + hs.k;
+      }
+      // position of the count-th draw start
+      // starts are all positions not inside a skip run; the j-th start (0-based) is at
+      // j + (skipped raws before it).  Walk the skip runs to locate start `count - 1`.
+      int64_t before = 0;  // skipped raws before the current position
+      int64_t end_pos = -1;
+      {
+        int64_t target = count - 1;  // draw index
+        size_t r = 0;
+        int64_t cur = 0;  // candidate position = target + before
+        for (;;) {
+          cur = target + before;
+          if (r < skip_begin.size() && skip_begin[r] <= cur) {
+            before += skip_len[r];
+            ++r;
+            continue;
+          }
+          break;
+        }
+        end_pos = cur;
+      }
+      if (end_pos >= m) continue;  // not enough raws generated: retry with more
+      // consumption of the last draw
+      int64_t cons = 1;
+      auto itp = std::lower_bound(sp_pos.begin(), sp_pos.end(), end_pos);
+      if (itp != sp_pos.end() && *itp == end_pos) {
+        // its consumption is recorded in the skip run that follows it (if any)
+        auto itb = std::lower_bound(skip_begin.begin(), skip_begin.end(), end_pos + 1);
+        if (itb != skip_begin.end() && *itb == end_pos + 1) cons = 1 + skip_len[itb - skip_begin.begin()];
+      }
+      // device: mask skipped positions, number the starts, emit
+      Scratch is_start(sizeof(uint32_t) * m, s), index(sizeof(uint32_t) * m, s);
+      k_init_starts<<<(int)std::min<int64_t>((m + 255) / 256, 65535), 256, 0, s>>>(m, is_start.as<uint32_t>());
+      CSC_LAUNCHED();
+      const int64_t nskip = (int64_t)skip_begin.size();
+      Scratch dsb(sizeof(int64_t) * std::max<int64_t>(nskip, 1), s), dsl(sizeof(int32_t) * std::max<int64_t>(nskip, 1), s);
+      if (nskip) {
+        CSC_CUDA(cudaMemcpyAsync(dsb.get(), skip_begin.data(), sizeof(int64_t) * nskip, cudaMemcpyHostToDevice, s));
+        CSC_CUDA(cudaMemcpyAsync(dsl.get(), skip_len.data(), sizeof(int32_t) * nskip, cudaMemcpyHostToDevice, s));
+        k_mark_skips<<<(int)std::min<int64_t>((nskip + 255) / 256, 65535), 256, 0, s>>>(
+            dsb.as<int64_t>(), dsl.as<int32_t>(), nskip, m, is_start.as<uint32_t>());
+        CSC_LAUNCHED();
+      }
+      size_t tb2 = 0;
+      CSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
+      Scratch tmp2(tb2, s);
+      CSC_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.get(), tb2, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
+      CSC_LAUNCHED();
+      const int64_t nsp = (int64_t)sp_pos.size();
+      Scratch dsp(sizeof(int64_t) * std::max<int64_t>(nsp, 1), s), dsv(sizeof(double) * std::max<int64_t>(nsp, 1), s);
+      if (nsp) {
+        CSC_CUDA(cudaMemcpyAsync(dsp.get(), sp_pos.data(), sizeof(int64_t) * nsp, cudaMemcpyHostToDevice, s));
+        CSC_CUDA(cudaMemcpyAsync(dsv.get(), sp_val.data(), sizeof(double) * nsp, cudaMemcpyHostToDevice, s));
+      }
+      k_emit<<<(int)std::min<int64_t>((m + 255) / 256, 65535), 256, 0, s>>>(
+          raw.as<uint64_t>(), special.as<uint8_t>(), is_start.as<uint32_t>(), index.as<uint32_t>(), m, count,
+          dsp.as<int64_t>(), dsv.as<double>(), nsp, divisor, dout.as<double>());
+      CSC_LAUNCHED();
+      dout.finish();
+      CSC_CUDA(cudaStreamSynchronize(s));
+      *raw_consumed = end_pos + cons;
+      return;
+    }
+    fail(CSC_ERR_CUDA, "parity RNG: raw margin exhausted");
+  });
+}
+
+}  // extern "C"

@@ -180,3 +180,17 @@ def test_ari():
     assert P.adjusted_rand_index(a, a) == 1.0
     assert P.adjusted_rand_index(a, np.array([5, 5, 3, 3, 1, 1])) == 1.0
     assert abs(P.adjusted_rand_index(a, np.array([0, 1, 0, 1, 0, 1]))) < 0.5
+
+
+def test_numpy_ziggurat_restatement():
+    """Tables read from numpy's binary + the restated PCG64/ziggurat reproduce numpy (incl. slow paths)."""
+    from paper_1602_02018_b200 import _npzig as Z
+
+    ki, wi, fi = Z.ziggurat_tables()  # verifies internally on 2 x 20000 draws
+    rng = np.random.default_rng(99)
+    s, inc = Z.pcg_state(rng)
+    ns = Z.NormalStream(s, inc, (ki, wi, fi))
+    got = np.array([ns.normal() for _ in range(50_000)])
+    assert np.array_equal(got, rng.standard_normal(50_000))
+    assert (ns.s, ns.inc) == Z.pcg_state(rng)
+    assert ns.raw_count > 50_000  # slow paths consumed extra raws
