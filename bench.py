@@ -225,15 +225,18 @@ def run_ours(args, cfg):
     csc = None
     lam = 0.5
     if world == 1 and not args.no_csc:
-        t0 = time.perf_counter()
-        res = P.run_csc(op, P.CscParams(k=k, d=d, seed=0))
-        wall = time.perf_counter() - t0
+        walls = []
+        for _ in range(2):  # first call pays one-off module loading / pool growth; report both
+            t0 = time.perf_counter()
+            res = P.run_csc(op, P.CscParams(k=k, d=d, seed=0))
+            walls.append(time.perf_counter() - t0)
         lam = res.diagnostics["lambda_k_hat"]
-        csc = {"wall_s": wall, "stages_s": res.diagnostics["timings"], "lambda_k_hat": lam,
-               "probe_iterations": res.diagnostics["probe_iterations"],
+        csc = {"wall_s": walls[1], "wall_s_first_call": walls[0], "stages_s": res.diagnostics["timings"],
+               "lambda_k_hat": lam, "probe_iterations": res.diagnostics["probe_iterations"],
                "cg_iterations_max": max(res.diagnostics["solver_iterations"]),
                "ari_vs_truth": P.adjusted_rand_index(truth, res.labels), "dtype": cfg["dtype"],
-               "note": "full run_csc incl. host numpy RNG (parity mode), timed once before the bench"}
+               "note": "full run_csc in parity mode (numpy's seeded streams reproduced on the GPU), "
+                       "graph resident; second call timed"}
         del res
     filt = P.design_lowpass(lam, P_ORDER)
 

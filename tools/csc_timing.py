@@ -1,0 +1,27 @@
+"""Time run_csc at a BASELINE config several times (cold + warm) with stage timings."""
+import argparse
+import json
+import math
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from bench import CONFIGS, make_graph  # noqa: E402
+import paper_1602_02018_b200 as P  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c3")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--dtype", default=None)
+args = ap.parse_args()
+cfg = CONFIGS[args.config]
+g, truth = make_graph(P, cfg)
+op = P.laplacian_op(g, dtype=args.dtype or cfg["dtype"])
+d = int(math.ceil(4 * math.log(cfg["N"])))
+for r in range(args.reps):
+    t0 = time.perf_counter()
+    res = P.run_csc(op, P.CscParams(k=cfg["k"], d=d, seed=0))
+    wall = time.perf_counter() - t0
+    print(json.dumps({"rep": r, "wall_s": round(wall, 4), "stages": {k: round(v, 4) for k, v in res.diagnostics["timings"].items()},
+                      "lambda": res.diagnostics["lambda_k_hat"], "ari": round(P.adjusted_rand_index(truth, res.labels), 4)}), flush=True)
