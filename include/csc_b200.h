@@ -62,8 +62,15 @@ const char* csc_last_error(void);
 /* Number of CUDA kernels this library has launched in the process so far. */
 int csc_launch_count(int64_t* out);
 /* Tuning knobs (process-wide; not to be changed while calls are in flight):
- *   "panel_width"   columns per panel (0 = auto)      "recurrence"  0 Clenshaw, 1 forward
- *   "cache_hints"   1 streaming hints on, 0 off        "block_threads" threads per CTA
+ *   "panel_width"   columns per panel (0 = auto, degree- and L2-aware)
+ *   "recurrence"    0 Clenshaw (4 streams/step, default), 1 forward (5 streams/step)
+ *   "cache_hints"   1 evict-first hints on streamed operands, 0 off
+ *   "block_threads" threads per CTA (64..256)
+ *   "unroll"        neighbour gathers in flight per lane / occupancy: 4 (default: 4 in
+ *                   flight, 6 CTAs/SM), 2 (4 in flight, 8 CTAs/SM), 8 (8 in flight, 2 CTAs/SM)
+ *   "row_order"     0 interleaved row groups (default), 1 contiguous runs per warp
+ *   "l2_budget_pct" L2 share a gathered panel may use (auto panel width)
+ *   "l2_persist_pct" >0: persisting-L2 access window on the gathered panel
  *   "profile"       1 = time the Chebyshev step kernels with CUDA events            */
 int csc_set_option(const char* key, int64_t value);
 int csc_get_option(const char* key, int64_t* value);

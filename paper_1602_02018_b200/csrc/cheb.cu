@@ -763,24 +763,11 @@ __global__ void k_reduce_sum(const double* __restrict__ in, int64_t count, doubl
   if (threadIdx.x == 0) out[0] = red[0];
 }
 
-__global__ void k_reduce_cols(const double* __restrict__ in, int64_t nblocks, int stride, int ncols,
-                              double* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int64_t b = 0; b < nblocks; ++b) acc += in[b * stride + c];
-    out[c] = acc;
-  }
-}
-
 void reduce_sum(const double* in, int64_t count, double* out, cudaStream_t s) {
   k_reduce_sum<<<1, 256, 0, s>>>(in, count, out);
   CSC_LAUNCHED();
 }
 
-void reduce_cols(const double* in, int64_t nblocks, int stride, int ncols, double* out, cudaStream_t s) {
-  k_reduce_cols<<<(ncols + 127) / 128, 128, 0, s>>>(in, nblocks, stride, ncols, out);
-  CSC_LAUNCHED();
-}
 
 // features: sum the panel row norms in panel order, normalise, flag zero rows
 template <typename T, typename To>

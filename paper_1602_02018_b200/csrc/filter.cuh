@@ -115,7 +115,5 @@ void unpack_panels(const void* src, int dtype, const PanelPlan& pp, int64_t n, v
 
 // Deterministic fixed-order sum of `count` doubles into out[0] (device).
 void reduce_sum(const double* in, int64_t count, double* out, cudaStream_t s);
-// out[c] = sum_b in[b * stride + c] for c < ncols (fixed order).
-void reduce_cols(const double* in, int64_t nblocks, int stride, int ncols, double* out, cudaStream_t s);
 
 }  // namespace csc

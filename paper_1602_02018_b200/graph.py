@@ -251,11 +251,10 @@ class LaplacianOp:
 def laplacian_op(graph: Graph, dtype: str = "float64", device: int | None = None) -> LaplacianOp:
     """Build (and upload) the normalized Laplacian operator (reference graph.py:164-169)."""
     dev = _lib.default_device() if device is None else int(device)
-    dg = graph.device_graph(_lib.dtype_code(dtype), dev)
+    graph.device_graph(_lib.dtype_code(dtype), dev)  # upload + normalise now (K1), cached on the graph
     d = graph.degrees
     with np.errstate(divide="ignore"):
         dis = np.where(d > 0, 1.0 / np.sqrt(np.where(d > 0, d, 1.0)), 0.0)
-    del dg
     return LaplacianOp(graph=graph, d_inv_sqrt=dis, dtype=str(np.dtype(dtype)), device=dev)
 
 
