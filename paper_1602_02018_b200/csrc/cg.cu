@@ -105,14 +105,26 @@ struct ColState {
   int* nactive;    // device counter
 };
 
-// rs = ||B||^2, target^2, initial active set (sampling.py:150-153)
-__global__ void k_cg_init(const double* __restrict__ part, int64_t nblocks, int pw, int wc, double tol, ColState st) {
-  const int c = threadIdx.x;
-  if (c == 0) *st.nactive = 0;
-  __syncthreads();
-  if (c >= wc) return;
+// Fixed-order sum over the per-block partials of column c (one CTA per column):
+// thread t adds blocks t, t + 256, ... sequentially, then a fixed tree.
+__device__ double column_total(const double* __restrict__ part, int64_t nblocks, int pw, int c) {
+  __shared__ double red[256];
   double s = 0.0;
-  for (int64_t b = 0; b < nblocks; ++b) s += part[b * pw + c];
+  for (int64_t b = threadIdx.x; b < nblocks; b += blockDim.x) s += part[b * pw + c];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o >= 1; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  return red[0];
+}
+
+// rs = ||B||^2, target^2, initial active set (sampling.py:150-153); grid = wc CTAs
+__global__ void k_cg_init(const double* __restrict__ part, int64_t nblocks, int pw, int wc, double tol, ColState st) {
+  const int c = blockIdx.x;
+  const double s = column_total(part, nblocks, pw, c);
+  if (threadIdx.x != 0) return;
   st.rs[c] = s;
   const double t = tol * sqrt(s);
   st.t2[c] = t * t;
@@ -122,24 +134,22 @@ __global__ void k_cg_init(const double* __restrict__ part, int64_t nblocks, int 
   if (act) atomicAdd(st.nactive, 1);
 }
 
-// alpha = rs / (P.AP) on active columns with |denom| > tiny (sampling.py:159-160)
+// alpha = rs / (P.AP) on active columns with |denom| > tiny (sampling.py:159-160);
+// also clears the active counter that k_cg_beta refills
 __global__ void k_cg_alpha(const double* __restrict__ part, int64_t nblocks, int pw, int wc, ColState st) {
-  const int c = threadIdx.x;
-  if (c >= wc) return;
-  double d = 0.0;
-  for (int64_t b = 0; b < nblocks; ++b) d += part[b * pw + c];
+  const int c = blockIdx.x;
+  const double d = column_total(part, nblocks, pw, c);
+  if (threadIdx.x != 0) return;
+  if (c == 0) *st.nactive = 0;
   const bool ok = st.active[c] && fabs(d) > kTiny;
   st.alpha[c] = ok ? st.rs[c] / d : 0.0;
 }
 
 // beta, rs update, freeze newly converged columns (sampling.py:164-170)
 __global__ void k_cg_beta(const double* __restrict__ part, int64_t nblocks, int pw, int wc, int64_t iter, ColState st) {
-  const int c = threadIdx.x;
-  if (c == 0) *st.nactive = 0;
-  __syncthreads();
-  if (c >= wc) return;
-  double rsn = 0.0;
-  for (int64_t b = 0; b < nblocks; ++b) rsn += part[b * pw + c];
+  const int c = blockIdx.x;
+  const double rsn = column_total(part, nblocks, pw, c);
+  if (threadIdx.x != 0) return;
   const bool act = st.active[c] != 0;
   st.beta[c] = act ? rsn / fmax(st.rs[c], kTiny) : 0.0;
   st.rs[c] = rsn;
@@ -221,41 +231,37 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
   CSC_LAUNCHED();
   k_colsumsq<T><<<cg, 256, 0, s>>>(R.as<T>(), N, pw, wc, part.as<double>());
   CSC_LAUNCHED();
-  k_cg_init<<<1, 128, 0, s>>>(part.as<double>(), cg, pw, wc, tol, st);
+  CSC_CUDA(cudaMemsetAsync(st.nactive, 0, sizeof(int), s));
+  k_cg_init<<<wc, 256, 0, s>>>(part.as<double>(), cg, pw, wc, tol, st);
   CSC_LAUNCHED();
 
-  int* h_active = nullptr;
-  CSC_CUDA(cudaMallocHost(&h_active, sizeof(int)));
+  // per-thread pinned flag (cudaMallocHost/cudaFreeHost per call would synchronise the device)
+  static thread_local int* h_active = nullptr;
+  if (!h_active) CSC_CUDA(cudaMallocHost(&h_active, sizeof(int)));
   int64_t iters = 0;
-  try {
+  CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CSC_CUDA(cudaStreamSynchronize(s));
+  while (*h_active > 0 && iters < max_iters) {
+    EpiExtra ex;
+    ex.part = part.as<double>();
+    ex.mask = mask;
+    ex.gamma = gamma;
+    ex.ridge = ridge;
+    ex.ap = AP.get();
+    const int fgrid = filter_panel<T>(g, hp, nc, P.as<T>(), Ps.as<T>(), nullptr, B0.as<T>(), B1.as<T>(),
+                                      Yacc.as<T>(), pw, wc, EPI_CGAP, ex, s);
+    k_cg_alpha<<<wc, 256, 0, s>>>(part.as<double>(), fgrid, pw, wc, st);
+    CSC_LAUNCHED();
+    k_cg_update<T><<<cg, 256, 0, s>>>(Xp, R.as<T>(), P.as<T>(), AP.as<T>(), st.alpha, N, pw, wc, part.as<double>());
+    CSC_LAUNCHED();
+    ++iters;
+    k_cg_beta<<<wc, 256, 0, s>>>(part.as<double>(), cg, pw, wc, iters, st);
+    CSC_LAUNCHED();
+    k_cg_direction<T><<<dgrid, 256, 0, s>>>(P.as<T>(), Ps.as<T>(), R.as<T>(), st.beta, g->dis, N, pw, wc);
+    CSC_LAUNCHED();
     CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
     CSC_CUDA(cudaStreamSynchronize(s));
-    while (*h_active > 0 && iters < max_iters) {
-      EpiExtra ex;
-      ex.part = part.as<double>();
-      ex.mask = mask;
-      ex.gamma = gamma;
-      ex.ridge = ridge;
-      ex.ap = AP.get();
-      const int fgrid = filter_panel<T>(g, hp, nc, P.as<T>(), Ps.as<T>(), nullptr, B0.as<T>(), B1.as<T>(),
-                                        Yacc.as<T>(), pw, wc, EPI_CGAP, ex, s);
-      k_cg_alpha<<<1, 128, 0, s>>>(part.as<double>(), fgrid, pw, wc, st);
-      CSC_LAUNCHED();
-      k_cg_update<T><<<cg, 256, 0, s>>>(Xp, R.as<T>(), P.as<T>(), AP.as<T>(), st.alpha, N, pw, wc, part.as<double>());
-      CSC_LAUNCHED();
-      ++iters;
-      k_cg_beta<<<1, 128, 0, s>>>(part.as<double>(), cg, pw, wc, iters, st);
-      CSC_LAUNCHED();
-      k_cg_direction<T><<<dgrid, 256, 0, s>>>(P.as<T>(), Ps.as<T>(), R.as<T>(), st.beta, g->dis, N, pw, wc);
-      CSC_LAUNCHED();
-      CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
-      CSC_CUDA(cudaStreamSynchronize(s));
-    }
-  } catch (...) {
-    cudaFreeHost(h_active);
-    throw;
   }
-  cudaFreeHost(h_active);
   k_cg_finish<<<1, 128, 0, s>>>(st, wc, iters, resid, conv, its);
   CSC_LAUNCHED();
   *iters_run = std::max(*iters_run, iters);
