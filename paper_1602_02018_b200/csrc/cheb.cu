@@ -644,7 +644,9 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
         relax * (double)device_props(device).l2_bytes * (double)g_opt.l2_budget_pct.load() / 100.0;
     int pw = vec;
     while (pw * 2 <= max_pw && (double)n * (pw * 2) * dtype_size(dtype) <= budget) pw *= 2;
-    if ((double)n * pw * dtype_size(dtype) > budget) pw = max_pw;  // nothing fits: minimise CSR passes
+    // nothing fits: 8 lanes per row (32 fp32 / 16 fp64 columns) -- wider rows per lane
+    // group lose more than the CSR passes they save (measured at N = 16e6, d = 67)
+    if ((double)n * pw * dtype_size(dtype) > budget) pw = 8 * vec;
     max_pw = pw;
   }
   PanelPlan pp;
