@@ -97,9 +97,10 @@ def device_rng_available() -> bool:
     return _tables_loaded
 
 
-def device_normal_block(rng: np.random.Generator, n: int, w: int, device: int = 0, out=None):
+def device_normal_block(rng: np.random.Generator, n: int, w: int, device: int = 0, out=None, stream=None):
     """``rng.standard_normal((n, w)) / sqrt(w)`` drawn on the GPU into a CUDA fp64 tensor,
-    bit-identical to numpy; ``rng`` is advanced exactly as the host draw would advance it."""
+    bit-identical to numpy; ``rng`` is advanced exactly as the host draw would advance it.
+    ``stream``: a torch.cuda.Stream to run on (default: the current stream)."""
     import ctypes as C
 
     import torch
@@ -116,21 +117,38 @@ def device_normal_block(rng: np.random.Generator, n: int, w: int, device: int = 
     divisor = float(np.sqrt(w))
     _lib.call("csc_numpy_normals", C.c_uint64(state >> 64), C.c_uint64(state & ((1 << 64) - 1)),
               C.c_uint64(inc >> 64), C.c_uint64(inc & ((1 << 64) - 1)), int(n) * int(w), divisor, out.data_ptr(),
-              C.byref(consumed), int(device), _lib.current_stream(device))
+              C.byref(consumed), int(device), stream.cuda_stream if stream is not None else _lib.current_stream(device))
     rng.bit_generator.advance(int(consumed.value))
     return out
 
 
 class DeviceProbeStream:
-    """Sequential probe blocks drawn on the GPU (same values as ProbeStream)."""
+    """Sequential probe blocks drawn on the GPU (same values as ProbeStream), one block
+    ahead: a worker thread draws block t + 1 on its own CUDA stream (kernels + the host
+    walk of the rare slow paths) while the caller filters block t."""
 
     def __init__(self, rng: np.random.Generator, n: int, ds: int, device: int):
+        import torch
+
         self.rng, self.n, self.ds, self.device = rng, n, ds, device
-        self.buf = None
+        self.side = torch.cuda.Stream(device=device)
+        self.bufs = [torch.empty((n, ds), dtype=torch.float64, device=f"cuda:{device}") for _ in range(2)]
+        self.i = 0
+        self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="csc-probe-devrng")
+        self.next = self.pool.submit(self._draw, 0)
+
+    def _draw(self, slot: int):
+        return device_normal_block(self.rng, self.n, self.ds, self.device, self.bufs[slot], self.side)
 
     def take(self):
-        self.buf = device_normal_block(self.rng, self.n, self.ds, self.device, self.buf)
-        return self.buf
+        block = self.next.result()  # drawn and synchronised on the side stream
+        self.i += 1
+        # the caller's use of the previous block has finished (eigencount returns after a sync)
+        self.next = self.pool.submit(self._draw, self.i % 2)
+        return block
 
     def close(self) -> None:
-        pass
+        try:
+            self.next.result()
+        finally:
+            self.pool.shutdown(wait=True)

@@ -378,13 +378,15 @@ int csc_graph_build_coo(int64_t num_nodes, int64_t num_edges, const int64_t* src
         CSC_CUDA(cudaStreamSynchronize(s));
         auto edge_str = [&](unsigned long long e) {
           int64_t a, b;
-          CSC_CUDA(cudaMemcpy(&a, vs.as<int64_t>() + e, sizeof(a), cudaMemcpyDeviceToHost));
-          CSC_CUDA(cudaMemcpy(&b, vd.as<int64_t>() + e, sizeof(b), cudaMemcpyDeviceToHost));
+          CSC_CUDA(cudaMemcpyAsync(&a, vs.as<int64_t>() + e, sizeof(a), cudaMemcpyDeviceToHost, s));
+          CSC_CUDA(cudaMemcpyAsync(&b, vd.as<int64_t>() + e, sizeof(b), cudaMemcpyDeviceToHost, s));
+          CSC_CUDA(cudaStreamSynchronize(s));
           return std::make_pair(a, b);
         };
         if (hf[0] != ~0ull) {
           double wv;
-          CSC_CUDA(cudaMemcpy(&wv, vw.as<double>() + hf[0], sizeof(wv), cudaMemcpyDeviceToHost));
+          CSC_CUDA(cudaMemcpyAsync(&wv, vw.as<double>() + hf[0], sizeof(wv), cudaMemcpyDeviceToHost, s));
+          CSC_CUDA(cudaStreamSynchronize(s));
           auto ab = edge_str(hf[0]);
           fail(CSC_ERR_GRAPH, "negative weight " + std::to_string(wv) + " on edge (" + std::to_string(ab.first) +
                                   ", " + std::to_string(ab.second) + ")");

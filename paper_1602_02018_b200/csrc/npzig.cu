@@ -19,8 +19,12 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "internal.cuh"
@@ -188,6 +192,21 @@ double slow_draw(HostStream& hs, const Tables& t) {
   }
 }
 
+// grow-only pinned host staging, one per thread
+template <typename T>
+T* pinned_buffer(size_t count, int slot) {
+  static thread_local void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  static thread_local size_t cap[4] = {0, 0, 0, 0};
+  const size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
+  if (cap[slot] < bytes) {
+    if (buf[slot]) cudaFreeHost(buf[slot]);
+    buf[slot] = nullptr;
+    CSC_CUDA(cudaMallocHost(&buf[slot], bytes + bytes / 4));
+    cap[slot] = bytes + bytes / 4;
+  }
+  return static_cast<T*>(buf[slot]);
+}
+
 }  // namespace
 }  // namespace csc
 
@@ -212,12 +231,13 @@ int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
     if (count < 0) fail(CSC_ERR_INVALID, "count must be >= 0");
     if (!out && count > 0) fail(CSC_ERR_INVALID, "out is NULL");
     if (!raw_consumed) fail(CSC_ERR_INVALID, "raw_consumed is NULL");
-    Tables t;
+    Tables tab;
     {
       std::lock_guard<std::mutex> lk(g_tab_mu);
       if (!g_tab.set) fail(CSC_ERR_INVALID, "normal tables not set (csc_set_normal_tables)");
-      t = g_tab;
+      tab = g_tab;
     }
+    const Tables& t = tab;
     if (count == 0) {
       *raw_consumed = 0;
       return;
@@ -230,6 +250,10 @@ int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
     const u128 s0 = make128(state_hi, state_lo), inc = make128(inc_hi, inc_lo);
     DeviceOut dout(out, sizeof(double) * count, device, s);
 
+    const bool timing = std::getenv("CSC_RNG_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    auto t_start = now();
     int64_t m = count + count / 16 + 4096;  // ~2.2 % of raws are consumed inside slow paths
     for (int attempt = 0; attempt < 4; ++attempt, m = m * 2) {
       Scratch raw(sizeof(uint64_t) * m, s), special(m, s);
@@ -250,39 +274,58 @@ int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
       int64_t nspec = 0;
       CSC_CUDA(cudaMemcpyAsync(&nspec, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       CSC_CUDA(cudaStreamSynchronize(s));
-      std::vector<int64_t> hpos(nspec);
-      if (nspec) CSC_CUDA(cudaMemcpy(hpos.data(), pos.get(), sizeof(int64_t) * nspec, cudaMemcpyDeviceToHost));
+      auto t_gen = now();
+      int64_t* hpos = pinned_buffer<int64_t>(nspec, 0);
+      if (nspec) CSC_CUDA(cudaMemcpyAsync(hpos, pos.get(), sizeof(int64_t) * nspec, cudaMemcpyDeviceToHost, s));
       // raws following each special position (slow paths read a few more)
       constexpr int kNear = 8;
-      std::vector<uint64_t> hraw((size_t)nspec * kNear);
+      uint64_t* hraw = pinned_buffer<uint64_t>((size_t)nspec * kNear, 1);
+      Scratch gath(sizeof(uint64_t) * std::max<int64_t>(nspec * kNear, 1), s);
       if (nspec) {
-        Scratch gath(sizeof(uint64_t) * nspec * kNear, s);
         k_gather_near<<<(int)std::min<int64_t>((nspec * kNear + 255) / 256, 65535), 256, 0, s>>>(
             raw.as<uint64_t>(), pos.as<int64_t>(), nspec, m, kNear, gath.as<uint64_t>());
         CSC_LAUNCHED();
-        CSC_CUDA(cudaMemcpyAsync(hraw.data(), gath.get(), sizeof(uint64_t) * nspec * kNear, cudaMemcpyDeviceToHost, s));
-        CSC_CUDA(cudaStreamSynchronize(s));
+        CSC_CUDA(cudaMemcpyAsync(hraw, gath.get(), sizeof(uint64_t) * nspec * kNear, cudaMemcpyDeviceToHost, s));
       }
-      // sequential walk: which specials start a draw, their values and consumption
+      CSC_CUDA(cudaStreamSynchronize(s));
+      auto t_d2h = now();
+      // every special evaluated as if it started a draw (its value and consumption
+      // depend only on its own raws): in parallel host threads with the C library's
+      // exp / log1p, then a sequential pass keeps the real starts
+      std::vector<double> val(nspec);
+      std::vector<int32_t> cons_all(nspec);
+      {
+        const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, nspec / 8192));
+        std::vector<std::thread> pool;
+        auto work = [&](int t) {
+          for (int64_t q = t; q < nspec; q += nth) {
+            HostStream hs{hraw + q * kNear, std::min<int64_t>(kNear, m - hpos[q]), hpos[q], s0, inc};
+            val[q] = slow_draw(hs, tab);
+            cons_all[q] = (int32_t)hs.k;
+          }
+        };
+        for (int t = 1; t < nth; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
+      }
       std::vector<int64_t> sp_pos, skip_begin;
       std::vector<double> sp_val;
       std::vector<int32_t> skip_len;
       int64_t next_free = 0, skipped = 0;
       for (int64_t q = 0; q < nspec; ++q) {
         const int64_t p = hpos[q];
-        if (p < next_free) continue;    // consumed by an earlier slow path
+        if (p < next_free) continue;      // consumed by an earlier slow path
         if (p - skipped >= count) break;  // draws before p already complete the request
-        HostStream hs{hraw.data() + q * kNear, std::min<int64_t>(kNear, m - p), p, s0, inc};
-        const double v = slow_draw(hs, t);
         sp_pos.push_back(p);
-        sp_val.push_back(v);
-        if (hs.k > 1) {
+        sp_val.push_back(val[q]);
+        if (cons_all[q] > 1) {
           skip_begin.push_back(p + 1);
-          skip_len.push_back((int32_t)(hs.k - 1));
-          skipped += hs.k - 1;
+          skip_len.push_back(cons_all[q] - 1);
+          skipped += cons_all[q] - 1;
         }
-        next_free = p + hs.k;
+        next_free = p + cons_all[q];
       }
+      auto t_walk = now();
       // position of the count-th draw start
       // starts are all positions not inside a skip run; the j-th start (0-based) is at
       // j + (skipped raws before it).  Walk the skip runs to locate start `count - 1`.
@@ -342,6 +385,10 @@ int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
       CSC_LAUNCHED();
       dout.finish();
       CSC_CUDA(cudaStreamSynchronize(s));
+      if (timing)
+        std::fprintf(stderr, "csc_numpy_normals: n=%lld specials=%lld gen %.2f d2h %.2f walk %.2f emit %.2f ms\n",
+                     (long long)count, (long long)nspec, ms(t_start, t_gen), ms(t_gen, t_d2h), ms(t_d2h, t_walk),
+                     ms(t_walk, now()));
       *raw_consumed = end_pos + cons;
       return;
     }
