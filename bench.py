@@ -250,8 +250,10 @@ def run_ours(args, cfg):
     backend = DeviceBackend(op)
     stream = torch.cuda.current_stream()
 
+    sharded = world > 1 or args.force_sharded
+
     def step_device():
-        if world == 1:
+        if not sharded:
             from paper_1602_02018_b200.features import features_into
 
             features_into(op, filt, X, F)
@@ -300,7 +302,7 @@ def run_ours(args, cfg):
     signals = RandomSignals(matrix=host, distribution="gaussian", seed=None)
 
     def step_e2e():
-        if world == 1:
+        if not sharded:
             build_features(op, filt, signals, out=rows_out)
         else:
             Xh = torch.from_numpy(host).to(f"cuda:{local}").to(dtype_t)
@@ -375,6 +377,8 @@ def main():
     ap.add_argument("--no-csc", action="store_true", help="skip the one-off full run_csc wall-time")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--option", action="append", default=[], help="libcsc option key=value (tuning)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the multi-GPU (column-sharded, NCCL) step even on one rank (path check)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
