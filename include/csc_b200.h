@@ -179,11 +179,30 @@ int csc_assign(const void* soft, int64_t ld, int64_t num_rows, int k, int io_dty
  * first-minimum labels, mean updates, farthest-point repair of empty clusters and
  * the relative-inertia stop (kmeans.py:64-93).  points n x d and init k x d are
  * row-major fp64 (host or device); labels_out int64[n], centroids_out k x d (may
- * be NULL), *inertia_out / *iters_out as the reference's Labeling fields.  The
- * k-means++ seeding stays on the host (numpy RNG, kmeans.py:46-61). */
+ * be NULL), *inertia_out / *iters_out as the reference's Labeling fields
+ * (kmeans(..., init=...), kmeans.py:110-114). */
 int csc_kmeans_lloyd(const double* points, int64_t n, int d, const double* init, int k, int64_t max_iters,
                      double tol, int64_t* labels_out, double* centroids_out, double* inertia_out, int64_t* iters_out,
                      int device, void* stream);
+
+/* `replicates` independent k-means runs, concurrently (one CTA each).  Seeding:
+ *   first_index != NULL: k-means++ (kmeans.py:52-61) -- replicate r's first
+ *     centroid is row first_index[r] (the host's rng.integers(q)) and its D^2
+ *     draws come from the PCG64 state pcg_states[4r..4r+3] = {state_hi, state_lo,
+ *     inc_hi, inc_lo} taken after that draw, with numpy's arithmetic (pairwise
+ *     sums, sequential cumsum, searchsorted 'right' of random());
+ *   first_index == NULL: init holds replicates x k x d starting centroids.
+ * Then Lloyd as csc_kmeans_lloyd.  Outputs per replicate: labels_out
+ * [replicates x n], centroids_out [replicates x k x d] (may be NULL),
+ * inertia_out / iters_out [replicates], status_out [replicates] (may be NULL):
+ * 0 = done, 1 = the D^2 total was not positive during seeding (the reference
+ * falls back to rng.integers there, kmeans.py:57-58): rerun that replicate with
+ * host seeding.  Replaces the replicate loop of kmeans (kmeans.py:117-124); the
+ * caller keeps the first lowest inertia. */
+int csc_kmeans_replicates(const double* points, int64_t n, int d, int k, int replicates, const int64_t* first_index,
+                          const uint64_t* pcg_states, const double* init, int64_t max_iters, double tol,
+                          int64_t* labels_out, double* centroids_out, double* inertia_out, int64_t* iters_out,
+                          int32_t* status_out, int device, void* stream);
 
 /* Column-sharded assign: for this rank's columns [col_offset, col_offset + k) of
  * the soft indicators, per row the best normalised value (fp64, -inf if every

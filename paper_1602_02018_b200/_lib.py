@@ -54,6 +54,7 @@ SIGNATURES: dict[str, list] = {
                      _p, _p, _p, _p, _p],
     "csc_assign": [_p, _i64, _i64, _i32, _i32, _p, _p, _p, _i32, _p],
     "csc_kmeans_lloyd": [_p, _i64, _i32, _p, _i32, _i64, _f64, _p, _p, _p, _p, _i32, _p],
+    "csc_kmeans_replicates": [_p, _i64, _i32, _i32, _i32, _p, _p, _p, _i64, _f64, _p, _p, _p, _p, _p, _i32, _p],
     "csc_set_normal_tables": [_p, _p, _p],
     "csc_numpy_normals": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i64, _f64, _p, _p, _i32, _p],
     "csc_comm_unique_id": [_p],

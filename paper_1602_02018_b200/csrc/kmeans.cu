@@ -1,155 +1,356 @@
-// K7: Lloyd iterations of the reduced k-means on the device (reference kmeans.py:64-93).
+// K7: the reduced k-means on the device (reference kmeans.py).
 //
-// One call runs one replicate from given initial centroids (the k-means++ seeding
-// stays on the host, where it must consume numpy's generator exactly like the
-// reference, kmeans.py:46-61).  Per iteration:
-//   k_sqnorm     |c_j|^2 in numpy's pairwise-summation order
-//   k_assign     D_ij = max(|p_i|^2 + |c_j|^2 - 2 p_i.c_j, 0) (kmeans.py:39-43); labels =
-//                first argmin; point_d2; one warp per point
-//   k_inertia    sum of point_d2 in numpy's pairwise order (kmeans.py:76)
-//   k_update     centroid_j = mean of its points, summed in point order (kmeans.py:80-82)
-//   repair       empty clusters take the farthest point, successively (kmeans.py:84-88)
-// The convergence test (kmeans.py:89-92) runs on the host on the returned inertia.
+// One CTA per replicate runs the whole replicate without returning to the host:
+//   seeding   k-means++ D^2 sampling with numpy's arithmetic (kmeans.py:46-61):
+//             d2 = ((P - c)**2).sum(axis=1) and d2.sum() in numpy's pairwise order,
+//             rng.choice(q, p=d2/total) == searchsorted(cumsum(p)/cumsum(p)[-1],
+//             random(), 'right') with random() drawn from the replicate's PCG64
+//             state (the first centroid, rng.integers(q), is drawn on the host);
+//   Lloyd     (kmeans.py:64-93) per iteration: |c_j|^2; D_ij = max(|p_i|^2 + |c_j|^2
+//             - 2 p_i.c_j, 0) (kmeans.py:39-43), first argmin; inertia = pairwise sum;
+//             centroid_j = mean of its points summed in point order; empty clusters
+//             take the farthest point, successively; relative-inertia stop.
+// Replicates run concurrently on separate SMs; the host picks the lowest inertia
+// (first minimum, kmeans.py:121-123).  A replicate whose D^2 total is not positive
+// (the reference's rng.integers fallback, kmeans.py:57-58) is flagged for the host.
 #include <cmath>
 #include <vector>
 
 #include "internal.cuh"
+#include "pcg64.cuh"
 
 namespace csc {
 namespace {
 
-// numpy's add-reduce order over a contiguous run (see graph.cu)
-__device__ double pairwise(const double* a, int64_t n, int64_t stride) {
+// numpy's pairwise add-reduce of v(off .. off+n-1) (numpy pairwise_sum; see graph.cu).
+// Products are rounded before the adds (__dmul_rn / __dadd_rn: no FMA contraction).
+template <class F>
+__device__ double pw_leaf(const F& v, int64_t off, int64_t n) {  // n <= 128
   if (n < 8) {
     double r = 0.0;
-    for (int64_t i = 0; i < n; ++i) r += a[i * stride];
+    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, v(off + i));
     return r;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = a[j * stride];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] += a[(i + j) * stride];
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res += a[i * stride];
-    return res;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return pairwise(a, n2, stride) + pairwise(a + n2 * stride, n - n2, stride);
-}
-
-// |row|^2 with the squares summed in numpy's order: (x*x).sum(axis=1) squares
-// first, then a pairwise reduction of the squared row
-__device__ double sq_row(const double* x, int d) {
-  double buf[8];
-  // reproduce pairwise() on the squared values without materialising them
-  if (d < 8) {
-    double r = 0.0;
-    for (int i = 0; i < d; ++i) r += x[i] * x[i];
-    return r;
-  }
-  if (d <= 128) {
-    for (int j = 0; j < 8; ++j) buf[j] = x[j] * x[j];
-    int i = 8;
-    for (; i < d - (d % 8); i += 8)
-      for (int j = 0; j < 8; ++j) buf[j] += x[i + j] * x[i + j];
-    double res = ((buf[0] + buf[1]) + (buf[2] + buf[3])) + ((buf[4] + buf[5]) + (buf[6] + buf[7]));
-    for (; i < d; ++i) res += x[i] * x[i];
-    return res;
-  }
-  int n2 = d / 2;
-  n2 -= n2 % 8;
-  return sq_row(x, n2) + sq_row(x + n2, d - n2);
-}
-
-__global__ void k_sqnorm(const double* __restrict__ X, int rows, int d, double* __restrict__ out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
-    out[i] = sq_row(X + (int64_t)i * d, d);
-}
-
-// one warp per point: distances to all centroids, first argmin
-__global__ void k_assign(const double* __restrict__ P, const double* __restrict__ pp, const double* __restrict__ C,
-                         const double* __restrict__ cc, int n, int k, int d, int64_t* __restrict__ labels,
-                         double* __restrict__ pd2) {
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = warp; i < n; i += nw) {
-    const double* p = P + (int64_t)i * d;
-    double best = INFINITY;
-    int bj = 0;
-    for (int j0 = 0; j0 < k; j0 += 32) {
-      const int j = j0 + lane;
-      double dist = INFINITY;
-      if (j < k) {
-        const double* c = C + (int64_t)j * d;
-        double dot = 0.0;
-        for (int t = 0; t < d; ++t) dot = fma(p[t], c[t], dot);
-        dist = fmax(pp[i] + cc[j] - 2.0 * dot, 0.0);
-      }
-      // warp argmin with first-index ties
-      double v = dist;
-      int vj = j < k ? j : INT_MAX;
+  double r[8];
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, vj, o);
-        if (ov < v || (ov == v && oj < vj)) {
-          v = ov;
-          vj = oj;
+  for (int j = 0; j < 8; ++j) r[j] = v(off + j);
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v(off + i + j));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, v(off + i));
+  return res;
+}
+
+// The recursion sum(a, n2) + sum(a + n2, n - n2), n2 = n/2 rounded down to a multiple
+// of 8, walked iteratively (device recursion would need a dynamic stack).
+template <class F>
+__device__ double pw_sum(const F& v, int64_t off, int64_t n) {
+  if (n <= 128) return pw_leaf(v, off, n);
+  int64_t fo[32], fn[32];
+  double left[32];
+  int st[32];
+  int sp = 0;
+  fo[0] = off;
+  fn[0] = n;
+  st[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    int64_t n2 = fn[sp] / 2;
+    n2 -= n2 % 8;
+    if (st[sp] == 0) {  // left half
+      st[sp] = 1;
+      if (n2 > 128) {
+        ++sp;
+        fo[sp] = fo[sp - 1];
+        fn[sp] = n2;
+        st[sp] = 0;
+        continue;
+      }
+      ret = pw_leaf(v, fo[sp], n2);
+    }
+    if (st[sp] == 1) {  // ret = left sum; right half
+      left[sp] = ret;
+      st[sp] = 2;
+      if (fn[sp] - n2 > 128) {
+        ++sp;
+        fo[sp] = fo[sp - 1] + n2;
+        fn[sp] = fn[sp - 1] - n2;
+        st[sp] = 0;
+        continue;
+      }
+      ret = pw_leaf(v, fo[sp] + n2, fn[sp] - n2);
+    }
+    ret = __dadd_rn(left[sp], ret);  // ret = right sum
+    --sp;
+  }
+  return ret;
+}
+
+// (x * x).sum() of one row
+__device__ double sq_row(const double* x, int d) {
+  return pw_sum([x](int64_t t) { return __dmul_rn(x[t], x[t]); }, 0, d);
+}
+
+// ((a - b) ** 2).sum() of one row
+__device__ double sqdiff_row(const double* a, const double* b, int d) {
+  return pw_sum([a, b](int64_t t) {
+    const double u = __dsub_rn(a[t], b[t]);
+    return __dmul_rn(u, u);
+  }, 0, d);
+}
+
+__global__ void k_sqnorm(const double* __restrict__ X, int64_t rows, int d, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = sq_row(X + i * d, d);
+}
+
+constexpr int kThreads = 512;
+
+struct RepScratch {
+  double* C;      // k x d centroids (global slice, used when they do not fit in shared memory)
+  double* near;   // n: D^2 of the seeding / point_d2 of Lloyd
+  double* cdf;    // n
+  int* lab;       // n
+  int* members;   // n: point indices grouped by cluster, point order within a cluster
+};
+
+__global__ void __launch_bounds__(kThreads) k_kmeans_rep(
+    const double* __restrict__ P, const double* __restrict__ pp, int64_t n, int d, int k, const int64_t* first,
+    const uint64_t* pcg, const double* init, int64_t max_iters, double tol, double* Cg, double* near_g, double* cdf_g,
+    int* lab_g, int* mem_g, int c_in_smem, int64_t* labels_out, double* centroids_out, double* inertia_out,
+    int64_t* iters_out, int* status_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int r = blockIdx.x, tid = threadIdx.x;
+  double* cc = reinterpret_cast<double*>(smem_raw);  // k
+  int* counts = reinterpret_cast<int*>(cc + k);      // k
+  int* offs = counts + k;                            // k
+  double* C = c_in_smem ? reinterpret_cast<double*>(smem_raw + (((size_t)k * 16 + 15) / 16) * 16)
+                        : Cg + (int64_t)r * k * d;
+  double* near = near_g + (int64_t)r * n;
+  double* cdf = cdf_g + (int64_t)r * n;
+  int* lab = lab_g + (int64_t)r * n;
+  int* members = mem_g + (int64_t)r * n;
+  __shared__ int64_t s_pick;
+  __shared__ double s_inertia;
+  __shared__ int s_rep;
+  int status = 0;
+
+  if (first) {
+    // ---- k-means++ seeding (kmeans.py:52-61)
+    u128 st = 0, inc = 0;
+    if (tid == 0) {
+      st = make128(pcg[4 * r], pcg[4 * r + 1]);
+      inc = make128(pcg[4 * r + 2], pcg[4 * r + 3]);
+    }
+    const double* p0 = P + first[r] * d;
+    for (int t = tid; t < d; t += kThreads) C[t] = p0[t];
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += kThreads) near[i] = sqdiff_row(P + i * d, C, d);
+    __syncthreads();
+    for (int j = 1; j < k; ++j) {
+      if (tid == 0) {
+        const double total = pw_sum([near](int64_t i) { return near[i]; }, 0, n);
+        s_pick = (total > 0.0 && total < INFINITY) ? 0 : -1;
+        s_inertia = total;
+      }
+      __syncthreads();
+      if (s_pick < 0) {
+        status = 1;
+        break;
+      }
+      const double total = s_inertia;
+      for (int64_t i = tid; i < n; i += kThreads) cdf[i] = __ddiv_rn(near[i], total);  // p = d2 / total
+      __syncthreads();
+      if (tid == 0) {
+        double acc = 0.0;  // cdf = p.cumsum() (sequential)
+        for (int64_t i = 0; i < n; ++i) {
+          acc = __dadd_rn(acc, cdf[i]);
+          cdf[i] = acc;
+        }
+        const double u = pcg_next_double(st, inc);
+        // searchsorted(cdf / cdf[-1], u, side='right'): first i with cdf[i]/last > u
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ddiv_rn(cdf[mid], acc) <= u) lo = mid + 1;
+          else hi = mid;
+        }
+        s_pick = lo;
+      }
+      __syncthreads();
+      const double* pj = P + s_pick * d;
+      double* cj = C + (int64_t)j * d;
+      for (int t = tid; t < d; t += kThreads) cj[t] = pj[t];
+      __syncthreads();
+      for (int64_t i = tid; i < n; i += kThreads) near[i] = fmin(near[i], sqdiff_row(P + i * d, cj, d));
+      __syncthreads();
+    }
+  } else {
+    const double* ci = init + (int64_t)r * k * d;
+    for (int64_t u = tid; u < (int64_t)k * d; u += kThreads) C[u] = ci[u];
+    __syncthreads();
+  }
+
+  double inertia = INFINITY;
+  int64_t iters = 0;
+  if (status == 0) {
+    for (int64_t i = tid; i < n; i += kThreads) lab[i] = 0;
+    const double tiny = 2.2250738585072014e-308;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int64_t it = 0; it < max_iters; ++it) {
+      for (int j = tid; j < k; j += kThreads) {
+        cc[j] = sq_row(C + (int64_t)j * d, d);
+        counts[j] = 0;
+      }
+      __syncthreads();
+      // assignment: one warp per point, lanes over centroids, first argmin
+      for (int64_t i = warp; i < n; i += kThreads / 32) {
+        const double* p = P + i * d;
+        double best = INFINITY;
+        int bj = 0;
+        for (int j0 = 0; j0 < k; j0 += 32) {
+          const int j = j0 + lane;
+          double dist = INFINITY;
+          if (j < k) {
+            const double* c = C + (int64_t)j * d;
+            double dot = 0.0;
+            for (int t = 0; t < d; ++t) dot = fma(p[t], c[t], dot);
+            dist = fmax(__dsub_rn(__dadd_rn(pp[i], cc[j]), 2.0 * dot), 0.0);
+          }
+          double v = dist;
+          int vj = j < k ? j : INT_MAX;
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, vj, o);
+            if (ov < v || (ov == v && oj < vj)) {
+              v = ov;
+              vj = oj;
+            }
+          }
+          if (v < best) {  // strictly smaller: earlier chunks keep ties
+            best = v;
+            bj = vj;
+          }
+        }
+        if (lane == 0) {
+          lab[i] = bj;
+          near[i] = best;
+          atomicAdd(&counts[bj], 1);
         }
       }
-      if (v < best) {  // strictly smaller: earlier chunks keep ties
-        best = v;
-        bj = vj;
+      __syncthreads();
+      if (tid == 0) {
+        s_inertia = pw_sum([near](int64_t i) { return near[i]; }, 0, n);
+        int acc = 0;
+        for (int j = 0; j < k; ++j) {
+          offs[j] = acc;
+          acc += counts[j];
+        }
       }
-    }
-    if (lane == 0) {
-      labels[i] = bj;
-      pd2[i] = best;
-    }
-  }
-}
-
-__global__ void k_inertia(const double* __restrict__ pd2, int n, double* __restrict__ out) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = pairwise(pd2, n, 1);
-}
-
-// centroid_j[t] = sum over points with label j (in point order) / count_j; counts out
-__global__ void k_update(const double* __restrict__ P, const int64_t* __restrict__ labels, int n, int k, int d,
-                         double* __restrict__ C, int* __restrict__ counts) {
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < (int64_t)k * d;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(u / d), t = (int)(u % d);
-    double s = 0.0;
-    int cnt = 0;
-    for (int i = 0; i < n; ++i)
-      if (labels[i] == j) {
-        s += P[(int64_t)i * d + t];
-        ++cnt;
+      __syncthreads();
+      // members of each cluster in point order
+      for (int j = tid; j < k; j += kThreads) {
+        int pos = offs[j];
+        if (counts[j] > 0)
+          for (int64_t i = 0; i < n; ++i)
+            if (lab[i] == j) members[pos++] = (int)i;
       }
-    if (cnt > 0) C[u] = s / cnt;
-    if (t == 0) counts[j] = cnt;
+      __syncthreads();
+      // centroid_j = points[labels == j].mean(axis=0): sum in point order, then / count
+      for (int64_t u = tid; u < (int64_t)k * d; u += kThreads) {
+        const int j = (int)(u / d), t = (int)(u % d);
+        const int cnt = counts[j];
+        if (cnt > 0) {
+          const int* mj = members + offs[j];
+          double s = 0.0;
+          for (int m = 0; m < cnt; ++m) s = __dadd_rn(s, P[(int64_t)mj[m] * d + t]);
+          C[u] = __ddiv_rn(s, (double)cnt);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int rep = 0;
+        for (int j = 0; j < k; ++j) {
+          if (counts[j] > 0) continue;
+          int64_t far = 0;  // first argmax of point_d2
+          for (int64_t i = 1; i < n; ++i)
+            if (near[i] > near[far]) far = i;
+          for (int t = 0; t < d; ++t) C[(int64_t)j * d + t] = P[far * d + t];
+          near[far] = 0.0;
+          rep = 1;
+        }
+        s_rep = rep;
+      }
+      __syncthreads();
+      const double ni = s_inertia;
+      iters = it + 1;
+      const bool settled = inertia - ni <= tol * fmax(ni, tiny);
+      inertia = ni;
+      if (!s_rep && settled) break;
+      __syncthreads();  // s_inertia / s_rep reused next iteration
+    }
+  }
+  for (int64_t i = tid; i < n; i += kThreads) labels_out[(int64_t)r * n + i] = status == 0 ? lab[i] : 0;
+  if (centroids_out)
+    for (int64_t u = tid; u < (int64_t)k * d; u += kThreads) centroids_out[(int64_t)r * k * d + u] = C[u];
+  if (tid == 0) {
+    inertia_out[r] = inertia;
+    iters_out[r] = iters;
+    status_out[r] = status;
   }
 }
 
-// empty clusters: successively take the farthest point (first max), zero its distance
-__global__ void k_repair(const double* __restrict__ P, int n, int k, int d, const int* __restrict__ counts,
-                         double* __restrict__ pd2, double* __restrict__ C, int* __restrict__ repaired) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  int rep = 0;
-  for (int j = 0; j < k; ++j) {
-    if (counts[j] > 0) continue;
-    int far = 0;
-    for (int i = 1; i < n; ++i)
-      if (pd2[i] > pd2[far]) far = i;
-    for (int t = 0; t < d; ++t) C[(int64_t)j * d + t] = P[(int64_t)far * d + t];
-    pd2[far] = 0.0;
-    rep = 1;
-  }
-  *repaired = rep;
+void run_replicates(const double* points, int64_t n, int d, int k, int reps, const int64_t* first,
+                    const uint64_t* pcg, const double* init, int64_t max_iters, double tol, int64_t* labels_out,
+                    double* centroids_out, double* inertia_out, int64_t* iters_out, int32_t* status_out, int device,
+                    void* stream) {
+  if (n < 1 || d < 1 || k < 1 || reps < 1) fail(CSC_ERR_INVALID, "kmeans: n, d, k and replicates must be >= 1");
+  if (n < k) fail(CSC_ERR_INVALID, "need at least k points");
+  if (n > INT32_MAX) fail(CSC_ERR_INVALID, "kmeans: too many points");
+  if (!points || !labels_out || !inertia_out || !iters_out) fail(CSC_ERR_INVALID, "NULL buffer");
+  if (!first && !init) fail(CSC_ERR_INVALID, "kmeans: need either seeding states or initial centroids");
+  if (first && !pcg) fail(CSC_ERR_INVALID, "kmeans: seeding needs the PCG64 states");
+  if (max_iters < 0) fail(CSC_ERR_INVALID, "max_iters must be >= 0");
+  DeviceGuard dg(device);
+  ensure_pool(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (first)
+    for (int r = 0; r < reps; ++r)
+      if (first[r] < 0 || first[r] >= n) fail(CSC_ERR_INVALID, "kmeans: first centroid index out of range");
+  DeviceView dP(points, sizeof(double) * n * d, device, s);
+  DeviceView dFirst(first, first ? sizeof(int64_t) * reps : 0, device, s);
+  DeviceView dPcg(pcg, first ? sizeof(uint64_t) * 4 * reps : 0, device, s);
+  DeviceView dInit(first ? nullptr : init, first ? 0 : sizeof(double) * reps * k * d, device, s);
+  const size_t c_bytes = sizeof(double) * k * d;
+  const size_t head = (((size_t)k * 16 + 15) / 16) * 16;  // cc + counts + offs
+  const bool c_smem = head + c_bytes <= 200 * 1024;
+  const size_t smem = head + (c_smem ? c_bytes : 0);
+  Scratch pp(sizeof(double) * n, s), Cg(c_smem ? 16 : c_bytes * reps, s), near(sizeof(double) * n * reps, s),
+      cdf(sizeof(double) * n * reps, s), lab(sizeof(int) * n * reps, s), mem(sizeof(int) * n * reps, s),
+      inert(sizeof(double) * reps, s), its(sizeof(int64_t) * reps, s), st(sizeof(int) * reps, s);
+  DeviceOut dLab(labels_out, sizeof(int64_t) * n * reps, device, s);
+  DeviceOut dCen(centroids_out, centroids_out ? c_bytes * reps : 0, device, s);
+  k_sqnorm<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(dP.as<double>(), n, d, pp.as<double>());
+  CSC_LAUNCHED();
+  CSC_CUDA(cudaFuncSetAttribute(k_kmeans_rep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_kmeans_rep<<<reps, kThreads, smem, s>>>(
+      dP.as<double>(), pp.as<double>(), n, d, k, first ? dFirst.as<int64_t>() : nullptr,
+      first ? dPcg.as<uint64_t>() : nullptr, first ? nullptr : dInit.as<double>(), max_iters, tol, Cg.as<double>(),
+      near.as<double>(), cdf.as<double>(), lab.as<int>(), mem.as<int>(), c_smem ? 1 : 0, dLab.as<int64_t>(),
+      centroids_out ? dCen.as<double>() : nullptr, inert.as<double>(), its.as<int64_t>(), st.as<int>());
+  CSC_LAUNCHED();
+  dLab.finish();
+  if (centroids_out) dCen.finish();
+  CSC_CUDA(cudaMemcpyAsync(inertia_out, inert.get(), sizeof(double) * reps, cudaMemcpyDefault, s));
+  CSC_CUDA(cudaMemcpyAsync(iters_out, its.get(), sizeof(int64_t) * reps, cudaMemcpyDefault, s));
+  std::vector<int32_t> hst(reps);
+  CSC_CUDA(cudaMemcpyAsync(hst.data(), st.get(), sizeof(int) * reps, cudaMemcpyDeviceToHost, s));
+  CSC_CUDA(cudaStreamSynchronize(s));
+  if (status_out) std::copy(hst.begin(), hst.end(), status_out);
 }
 
 }  // namespace
@@ -161,56 +362,23 @@ extern "C" int csc_kmeans_lloyd(const double* points, int64_t n, int d, const do
                                 double tol, int64_t* labels_out, double* centroids_out, double* inertia_out,
                                 int64_t* iters_out, int device, void* stream) {
   return guard([&] {
-    if (n < 1 || d < 1 || k < 1) fail(CSC_ERR_INVALID, "kmeans: n, d and k must be >= 1");
-    if (n < k) fail(CSC_ERR_INVALID, "need at least k points");
-    if (!points || !init || !labels_out) fail(CSC_ERR_INVALID, "NULL buffer");
-    if (max_iters < 0) fail(CSC_ERR_INVALID, "max_iters must be >= 0");
-    DeviceGuard dg(device);
-    ensure_pool(device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    DeviceView dP(points, sizeof(double) * n * d, device, s);
-    DeviceView dC0(init, sizeof(double) * k * d, device, s);
-    Scratch C(sizeof(double) * k * d, s), pp(sizeof(double) * n, s), cc(sizeof(double) * k, s),
-        pd2(sizeof(double) * n, s), inert(sizeof(double), s), counts(sizeof(int) * k, s), rep(sizeof(int), s);
-    DeviceOut lab(labels_out, sizeof(int64_t) * n, device, s);
-    CSC_CUDA(cudaMemcpyAsync(C.get(), dC0.as<double>(), sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
-    CSC_CUDA(cudaMemsetAsync(lab.as<int64_t>(), 0, sizeof(int64_t) * n, s));
-    const int ng = (int)std::min<int64_t>((n + 255) / 256, 1024);
-    k_sqnorm<<<ng, 256, 0, s>>>(dP.as<double>(), (int)n, d, pp.as<double>());
-    CSC_LAUNCHED();
-    const double tiny = 2.2250738585072014e-308;
-    double inertia = INFINITY;
+    if (!init) fail(CSC_ERR_INVALID, "NULL buffer");
+    double inertia = 0.0;
     int64_t iters = 0;
-    for (int64_t it = 0; it < max_iters; ++it) {
-      k_sqnorm<<<(k + 255) / 256, 256, 0, s>>>(C.as<double>(), k, d, cc.as<double>());
-      CSC_LAUNCHED();
-      k_assign<<<(int)std::min<int64_t>((n + 7) / 8, 2048), 256, 0, s>>>(dP.as<double>(), pp.as<double>(),
-                                                                          C.as<double>(), cc.as<double>(), (int)n, k,
-                                                                          d, lab.as<int64_t>(), pd2.as<double>());
-      CSC_LAUNCHED();
-      k_inertia<<<1, 32, 0, s>>>(pd2.as<double>(), (int)n, inert.as<double>());
-      CSC_LAUNCHED();
-      k_update<<<(int)std::min<int64_t>(((int64_t)k * d + 255) / 256, 4096), 256, 0, s>>>(
-          dP.as<double>(), lab.as<int64_t>(), (int)n, k, d, C.as<double>(), counts.as<int>());
-      CSC_LAUNCHED();
-      k_repair<<<1, 1, 0, s>>>(dP.as<double>(), (int)n, k, d, counts.as<int>(), pd2.as<double>(), C.as<double>(),
-                               rep.as<int>());
-      CSC_LAUNCHED();
-      double h_inert = 0.0;
-      int h_rep = 0;
-      CSC_CUDA(cudaMemcpyAsync(&h_inert, inert.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
-      CSC_CUDA(cudaMemcpyAsync(&h_rep, rep.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-      CSC_CUDA(cudaStreamSynchronize(s));
-      iters = it + 1;
-      const bool settled = inertia - h_inert <= tol * std::max(h_inert, tiny);
-      inertia = h_inert;
-      if (!h_rep && settled) break;
-    }
-    lab.finish();
-    if (centroids_out)
-      CSC_CUDA(cudaMemcpyAsync(centroids_out, C.get(), sizeof(double) * k * d, cudaMemcpyDefault, s));
-    CSC_CUDA(cudaStreamSynchronize(s));
+    run_replicates(points, n, d, k, 1, nullptr, nullptr, init, max_iters, tol, labels_out, centroids_out, &inertia,
+                   &iters, nullptr, device, stream);
     if (inertia_out) *inertia_out = inertia;
     if (iters_out) *iters_out = iters;
+  });
+}
+
+extern "C" int csc_kmeans_replicates(const double* points, int64_t n, int d, int k, int replicates,
+                                     const int64_t* first_index, const uint64_t* pcg_states, const double* init,
+                                     int64_t max_iters, double tol, int64_t* labels_out, double* centroids_out,
+                                     double* inertia_out, int64_t* iters_out, int32_t* status_out, int device,
+                                     void* stream) {
+  return guard([&] {
+    run_replicates(points, n, d, k, replicates, first_index, pcg_states, init, max_iters, tol, labels_out,
+                   centroids_out, inertia_out, iters_out, status_out, device, stream);
   });
 }

@@ -176,3 +176,71 @@ def test_kmeans_matches_oracle_random():
     a = P.kmeans(pts, P.KmeansConfig(k=5, seed=1, replicates=2))
     b = O.kmeans(pts, 5, 1, replicates=2)
     assert np.array_equal(a.labels, b[0]) and a.iterations_run == b[2]
+
+
+def _device_seeds(pts, k, children, max_iters=0):
+    from paper_1602_02018_b200 import _lib
+    from paper_1602_02018_b200.kmeans import _MASK64
+
+    n, d = pts.shape
+    R = len(children)
+    first = np.empty(R, dtype=np.int64)
+    pcg = np.empty((R, 4), dtype=np.uint64)
+    for r, ch in enumerate(children):
+        rng = np.random.default_rng(ch)
+        first[r] = rng.integers(n)
+        st = rng.bit_generator.state["state"]
+        pcg[r] = (st["state"] >> 64, st["state"] & _MASK64, st["inc"] >> 64, st["inc"] & _MASK64)
+    labels = np.empty((R, n), dtype=np.int64)
+    cent = np.empty((R, k, d))
+    inertia, iters = np.empty(R), np.empty(R, dtype=np.int64)
+    status = np.empty(R, dtype=np.int32)
+    _lib.call("csc_kmeans_replicates", _lib.ptr(pts), n, d, k, R, _lib.ptr(first), _lib.ptr(pcg), None, max_iters,
+              1e-6, _lib.ptr(labels), _lib.ptr(cent), _lib.ptr(inertia), _lib.ptr(iters), _lib.ptr(status), 0, None)
+    return cent, status, labels, inertia, iters
+
+
+@pytest.mark.parametrize("n,d,k", [(7, 3, 4), (922, 56, 100), (1000, 9, 30), (300, 130, 12)])
+def test_kmeanspp_seeding_bit_exact(n, d, k):
+    """Device D^2 sampling == the reference's numpy seeding (kmeans.py:52-61), bit for bit."""
+    rng = np.random.default_rng(n + d)
+    pts = rng.standard_normal((n, d)) * np.exp(rng.standard_normal((n, 1)))
+    children = np.random.SeedSequence(17).spawn(6)
+    cent, status, *_ = _device_seeds(pts, k, children)
+    assert np.all(status == 0)
+    for r, ch in enumerate(children):
+        ref = O._seed_kmeanspp(pts, k, np.random.default_rng(ch))
+        assert np.array_equal(cent[r], ref), r
+
+
+def test_kmeans_seeding_zero_total_flagged():
+    pts = np.repeat(np.eye(3), 4, axis=0)
+    _, status, *_ = _device_seeds(pts, 5, np.random.SeedSequence(1).spawn(3))
+    assert np.all(status == 1)
+
+
+def test_kmeans_replicates_large_k_global_centroids():
+    """k x d centroids beyond shared memory (global-memory path), many replicates."""
+    rng = np.random.default_rng(8)
+    k, d = 260, 100
+    centers = rng.normal(0, 10, (k, d))
+    pts = centers[rng.integers(k, size=1200)] + rng.normal(0, 0.5, (1200, d))
+    a = P.kmeans(pts, P.KmeansConfig(k=k, seed=4, replicates=3))
+    b = O.kmeans(pts, k, 4, replicates=3)
+    assert np.array_equal(a.labels, b[0]) and a.iterations_run == b[2]
+    assert abs(a.inertia - b[1]) <= 1e-9 * b[1]
+
+
+def test_kmeans_random_seeding_matches_host_replicates():
+    from paper_1602_02018_b200.kmeans import _initial_centers, _lloyd_device
+
+    rng = np.random.default_rng(12)
+    pts = np.concatenate([rng.normal(c, 0.4, (30, 4)) for c in range(5)])
+    cfg = P.KmeansConfig(k=5, seed=9, replicates=4, seeding="random")
+    a = P.kmeans(pts, cfg)
+    best = None
+    for ch in np.random.SeedSequence(9).spawn(4):
+        lab, inert, it = _lloyd_device(pts, _initial_centers(pts, 5, np.random.default_rng(ch), "random"), 100, 1e-6, 0)
+        if best is None or inert < best[1]:
+            best = (lab, inert, it)
+    assert np.array_equal(a.labels, best[0]) and a.inertia == best[1] and a.iterations_run == best[2]
