@@ -225,6 +225,28 @@ int csc_set_normal_tables(const uint64_t* ki, const double* wi, const double* fi
 int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
                       double divisor, double* out, int64_t* raw_consumed, int device, void* stream);
 
+/* numpy's 256-layer exponential ziggurat (ke uint64, we, fe fp64), for
+ * csc_sbm_edges. */
+int csc_set_exponential_tables(const uint64_t* ke, const double* we, const double* fe);
+
+/* Stochastic block model edges on the device, bit-identical to the reference's
+ * generator (sbm.py:83-100, 118-155) from the PCG64 state of
+ * default_rng(seed).  The npairs community pairs (a <= b, in the reference's
+ * order, pairs that draw nothing left out) each give: cells (candidate node
+ * pairs, > 0), log1m_q = log1p(-q) for its edge probability q in (0, 1/3)
+ * (computed by the caller with the C library, as numpy does), batch (the
+ * reference's gap batch size), diag (1 for a == b), row_first (first node of
+ * a), col_first / col_size (first node and size of b).  Edges are written in
+ * the reference's order, each pair once, as src[e] > dst[e] for diagonal pairs
+ * and src in a, dst in b otherwise; src/dst are int64 host or device buffers
+ * of `capacity` entries.  *num_edges receives the edge count (if it exceeds
+ * capacity: CSC_ERR_INVALID, nothing written); *raw_consumed the PCG64
+ * outputs used (may be NULL). */
+int csc_sbm_edges(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t npairs,
+                  const int64_t* cells, const double* log1m_q, const int64_t* batch, const int32_t* diag,
+                  const int64_t* row_first, const int64_t* col_first, const int64_t* col_size, int64_t capacity,
+                  int64_t* src, int64_t* dst, int64_t* num_edges, int64_t* raw_consumed, int device, void* stream);
+
 /* ---- row-sharded operator (BASELINE config 5) ------------- */
 /* NCCL communicator: rank 0 creates the id, the caller distributes it (e.g. a
  * torch.distributed broadcast), every rank creates its communicator. */

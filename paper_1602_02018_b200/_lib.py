@@ -57,6 +57,9 @@ SIGNATURES: dict[str, list] = {
     "csc_kmeans_replicates": [_p, _i64, _i32, _i32, _i32, _p, _p, _p, _i64, _f64, _p, _p, _p, _p, _p, _i32, _p],
     "csc_set_normal_tables": [_p, _p, _p],
     "csc_numpy_normals": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i64, _f64, _p, _p, _i32, _p],
+    "csc_set_exponential_tables": [_p, _p, _p],
+    "csc_sbm_edges": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p,
+                      _p, _p, _i32, _p],
     "csc_comm_unique_id": [_p],
     "csc_comm_create": [_p, _i32, _i32, _i32, _p],
     "csc_comm_destroy": [_p],

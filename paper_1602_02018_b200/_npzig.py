@@ -31,6 +31,7 @@ MASK128 = (1 << 128) - 1
 MASK64 = (1 << 64) - 1
 ZIG_R = 3.6541528853610087963519472518  # tail start of the 256-layer normal ziggurat
 ZIG_INV_R = 0.27366123732975827203338247596
+ZIG_EXP_R = 7.69711747013104972  # tail start of the 256-layer exponential ziggurat
 
 
 def _elf_symbols(path: str, names: set[str]) -> dict[str, bytes]:
@@ -61,6 +62,30 @@ def _elf_symbols(path: str, names: set[str]) -> dict[str, bytes]:
     return out
 
 
+def _find_tables(names: tuple[str, str, str]):
+    base = os.path.dirname(np.random.__file__)
+    for path in sorted(glob.glob(os.path.join(base, "_generator*.so"))) + sorted(glob.glob(os.path.join(base, "*.so"))):
+        try:
+            syms = _elf_symbols(path, set(names))
+        except (OSError, ValueError, struct.error):
+            continue
+        if len(syms) == 3 and all(len(v) == 2048 for v in syms.values()):
+            k, w, f = (syms[n] for n in names)
+            return (np.frombuffer(k, dtype="<u8").copy(), np.frombuffer(w, dtype="<f8").copy(),
+                    np.frombuffer(f, dtype="<f8").copy())
+    return None
+
+
+@lru_cache(maxsize=1)
+def exponential_tables() -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """(ke uint64[256], we float64[256], fe float64[256]) of the installed numpy, verified."""
+    tabs = _find_tables(("ke_double", "we_double", "fe_double"))
+    if tabs is None:
+        raise RuntimeError("numpy's exponential ziggurat tables were not found")
+    verify_exponential_tables(*tabs)
+    return tabs
+
+
 @lru_cache(maxsize=1)
 def ziggurat_tables() -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     """(ki uint64[256], wi float64[256], fi float64[256]) of the installed numpy."""
@@ -80,11 +105,14 @@ def ziggurat_tables() -> tuple[np.ndarray, np.ndarray, np.ndarray]:
 
 
 class NormalStream:
-    """numpy's Generator(PCG64).standard_normal, one draw at a time (pure Python)."""
+    """numpy's Generator(PCG64).standard_normal, one draw at a time (pure Python).
 
-    def __init__(self, state: int, inc: int, tables):
+    ``exp_tables`` enables ``exponential()`` / ``geometric()`` as well."""
+
+    def __init__(self, state: int, inc: int, tables, exp_tables=None):
         self.s, self.inc = state, inc
         self.ki, self.wi, self.fi = tables
+        self.ke, self.we, self.fe = exp_tables if exp_tables is not None else (None, None, None)
         self.raw_count = 0
 
     def next_u64(self) -> int:
@@ -120,6 +148,34 @@ class NormalStream:
                 return x
 
 
+    def exponential(self) -> float:
+        """numpy's random_standard_exponential (exponential ziggurat)."""
+        while True:
+            ri = self.next_u64() >> 3
+            idx = ri & 0xFF
+            ri >>= 8
+            x = ri * float(self.we[idx])
+            if ri < int(self.ke[idx]):
+                return x
+            if idx == 0:
+                return ZIG_EXP_R - math.log1p(-self.next_double())
+            if (float(self.fe[idx - 1]) - float(self.fe[idx])) * self.next_double() + float(self.fe[idx]) < math.exp(-x):
+                return x
+
+    def geometric(self, p: float) -> int:
+        """numpy's random_geometric: search for p >= 1/3, inversion otherwise."""
+        if p >= 0.333333333333333333333333:
+            x, total, prod, q = 1, p, p, 1.0 - p
+            u = self.next_double()
+            while u > total:
+                prod *= q
+                total += prod
+                x += 1
+            return x
+        z = math.ceil(-self.exponential() / math.log1p(-p))
+        return (1 << 63) - 1 if z >= 9.223372036854776e18 else int(z)
+
+
 def pcg_state(rng: np.random.Generator) -> tuple[int, int]:
     st = rng.bit_generator.state
     if st["bit_generator"] != "PCG64":
@@ -141,3 +197,15 @@ def verify_tables(ki, wi, fi, draws: int = 20000) -> None:
             raise RuntimeError("ziggurat tables do not reproduce numpy's standard_normal")
         if (ns.s, ns.inc) != pcg_state(rng):
             raise RuntimeError("PCG64 stream position diverged from numpy")
+
+
+def verify_exponential_tables(ke, we, fe, draws: int = 20000) -> None:
+    """The restated exponential / geometric draws must reproduce numpy's."""
+    for seed in (0, 12345):
+        rng = np.random.default_rng(seed)
+        s, inc = pcg_state(rng)
+        ref = rng.standard_exponential(draws)
+        ns = NormalStream(s, inc, (None, None, None), (ke, we, fe))
+        got = np.array([ns.exponential() for _ in range(draws)])
+        if not np.array_equal(got, ref) or (ns.s, ns.inc) != pcg_state(rng):
+            raise RuntimeError("exponential tables do not reproduce numpy's standard_exponential")

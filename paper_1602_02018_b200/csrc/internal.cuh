@@ -142,6 +142,11 @@ class Scratch {
   cudaStream_t s_ = nullptr;
 };
 
+// numpy Generator(PCG64).standard_exponential draws (bit-exact; npzig.cu) into
+// device memory; returns the raw uint64 consumed.
+int64_t numpy_exponentials(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                           double* out, cudaStream_t s);
+
 // Host or device?  Device pointers must belong to `device`.
 bool is_device_ptr(const void* p, int device);
 

@@ -35,21 +35,51 @@ namespace {
 
 constexpr double kZigR = 3.6541528853610087963519472518;
 constexpr double kZigInvR = 0.27366123732975827203338247596;
+constexpr double kZigExpR = 7.69711747013104972;  // tail start of the 256-layer exponential ziggurat
 
-__constant__ uint64_t c_ki[256];
+// which numpy distribution a stream of draws follows
+enum class Dist { Normal, Exponential };
+
+__constant__ uint64_t c_ki[256];  // normal:      ki / wi
 __constant__ double c_wi[256];
+__constant__ uint64_t c_ke[256];  // exponential: ke / we
+__constant__ double c_we[256];
 
 struct Tables {
-  uint64_t ki[256];
-  double wi[256];
-  double fi[256];
+  uint64_t k[256];
+  double w[256];
+  double f[256];
   bool set = false;
 };
-Tables g_tab;
+Tables g_tab, g_exp;
 std::mutex g_tab_mu;
+
+// the fast-path test of numpy's random_standard_normal / random_standard_exponential
+template <Dist D>
+__device__ inline bool is_special(uint64_t u) {
+  if (D == Dist::Normal) {
+    const uint64_t rabs = ((u >> 8) >> 1) & 0x000fffffffffffffull;
+    return rabs >= c_ki[u & 0xff];
+  } else {
+    return (u >> 11) >= c_ke[(u >> 3) & 0xff];
+  }
+}
+
+template <Dist D>
+__device__ inline double fast_value(uint64_t u) {
+  if (D == Dist::Normal) {
+    const uint64_t r = u >> 8;
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+    const double v = (double)rabs * c_wi[u & 0xff];
+    return (r & 1) ? -v : v;
+  } else {
+    return (double)(u >> 11) * c_we[(u >> 3) & 0xff];
+  }
+}
 
 constexpr int kChunk = 64;  // raws per thread
 
+template <Dist D>
 __global__ void k_pcg_raw(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, int64_t m,
                           uint64_t* __restrict__ raw, uint8_t* __restrict__ special) {
   const u128 inc = make128(i_hi, i_lo);
@@ -60,9 +90,7 @@ __global__ void k_pcg_raw(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t 
     for (int64_t i = i0; i < i1; ++i) {
       const uint64_t u = pcg_next(st, inc);
       raw[i] = u;
-      const unsigned idx = (unsigned)(u & 0xff);
-      const uint64_t rabs = ((u >> 8) >> 1) & 0x000fffffffffffffull;
-      special[i] = rabs >= c_ki[idx] ? 1 : 0;
+      special[i] = is_special<D>(u) ? 1 : 0;
     }
   }
 }
@@ -91,6 +119,7 @@ __global__ void k_init_starts(int64_t m, uint32_t* __restrict__ is_start) {
     is_start[i] = 1;
 }
 
+template <Dist D>
 __global__ void k_emit(const uint64_t* __restrict__ raw, const uint8_t* __restrict__ special,
                        const uint32_t* __restrict__ is_start, const uint32_t* __restrict__ index, int64_t m,
                        int64_t count, const int64_t* __restrict__ sp_pos, const double* __restrict__ sp_val,
@@ -111,12 +140,7 @@ __global__ void k_emit(const uint64_t* __restrict__ raw, const uint8_t* __restri
       }
       v = sp_val[lo];
     } else {
-      const uint64_t u = raw[i];
-      const unsigned idx = (unsigned)(u & 0xff);
-      const uint64_t r = u >> 8;
-      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-      v = (double)rabs * c_wi[idx];
-      if (r & 1) v = -v;
+      v = fast_value<D>(raw[i]);
     }
     out[j] = v / divisor;
   }
@@ -141,16 +165,17 @@ struct HostStream {
   double next_double() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); }
 };
 
-double slow_draw(HostStream& hs, const Tables& t) {
+// numpy's random_standard_normal, whole draw (fast and slow paths)
+double slow_normal(HostStream& hs, const Tables& t) {
   for (;;) {
     uint64_t r = hs.next();
     const int idx = (int)(r & 0xff);
     r >>= 8;
     const int sign = (int)(r & 1);
     const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-    double x = (double)rabs * t.wi[idx];
+    double x = (double)rabs * t.w[idx];
     if (sign) x = -x;
-    if (rabs < t.ki[idx]) return x;
+    if (rabs < t.k[idx]) return x;
     if (idx == 0) {
       for (;;) {
         const double xx = -kZigInvR * std::log1p(-hs.next_double());
@@ -158,9 +183,27 @@ double slow_draw(HostStream& hs, const Tables& t) {
         if (yy + yy > xx * xx) return ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
       }
     } else {
-      if ((t.fi[idx - 1] - t.fi[idx]) * hs.next_double() + t.fi[idx] < std::exp(-0.5 * x * x)) return x;
+      if ((t.f[idx - 1] - t.f[idx]) * hs.next_double() + t.f[idx] < std::exp(-0.5 * x * x)) return x;
     }
   }
+}
+
+// numpy's random_standard_exponential (standard_exponential_unlikely retries the whole draw)
+double slow_exponential(HostStream& hs, const Tables& t) {
+  for (;;) {
+    uint64_t ri = hs.next() >> 3;
+    const int idx = (int)(ri & 0xff);
+    ri >>= 8;
+    const double x = (double)ri * t.w[idx];
+    if (ri < t.k[idx]) return x;
+    if (idx == 0) return kZigExpR - std::log1p(-hs.next_double());
+    if ((t.f[idx - 1] - t.f[idx]) * hs.next_double() + t.f[idx] < std::exp(-x)) return x;
+  }
+}
+
+template <Dist D>
+double slow_draw(HostStream& hs, const Tables& t) {
+  return D == Dist::Normal ? slow_normal(hs, t) : slow_exponential(hs, t);
 }
 
 // grow-only pinned host staging, one per thread
@@ -178,49 +221,19 @@ T* pinned_buffer(size_t count, int slot) {
   return static_cast<T*>(buf[slot]);
 }
 
-}  // namespace
-}  // namespace csc
-
-using namespace csc;
-
-extern "C" {
-
-int csc_set_normal_tables(const uint64_t* ki, const double* wi, const double* fi) {
-  return guard([&] {
-    if (!ki || !wi || !fi) fail(CSC_ERR_INVALID, "NULL table");
-    std::lock_guard<std::mutex> lk(g_tab_mu);
-    std::memcpy(g_tab.ki, ki, sizeof(g_tab.ki));
-    std::memcpy(g_tab.wi, wi, sizeof(g_tab.wi));
-    std::memcpy(g_tab.fi, fi, sizeof(g_tab.fi));
-    g_tab.set = true;
-  });
-}
-
-int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
-                      double divisor, double* out, int64_t* raw_consumed, int device, void* stream) {
-  return guard([&] {
-    if (count < 0) fail(CSC_ERR_INVALID, "count must be >= 0");
-    if (!out && count > 0) fail(CSC_ERR_INVALID, "out is NULL");
-    if (!raw_consumed) fail(CSC_ERR_INVALID, "raw_consumed is NULL");
-    Tables tab;
-    {
-      std::lock_guard<std::mutex> lk(g_tab_mu);
-      if (!g_tab.set) fail(CSC_ERR_INVALID, "normal tables not set (csc_set_normal_tables)");
-      tab = g_tab;
-    }
-    const Tables& t = tab;
-    if (count == 0) {
-      *raw_consumed = 0;
-      return;
-    }
-    DeviceGuard dg(device);
-    ensure_pool(device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    CSC_CUDA(cudaMemcpyToSymbolAsync(c_ki, t.ki, sizeof(t.ki), 0, cudaMemcpyHostToDevice, s));
-    CSC_CUDA(cudaMemcpyToSymbolAsync(c_wi, t.wi, sizeof(t.wi), 0, cudaMemcpyHostToDevice, s));
-    const u128 s0 = make128(state_hi, state_lo), inc = make128(inc_hi, inc_lo);
-    DeviceOut dout(out, sizeof(double) * count, device, s);
-
+// The first `count` draws of numpy's Generator(PCG64) stream of distribution D
+// from state (s0, inc), divided by `divisor`, into device memory; returns the
+// number of raw uint64 the draws consumed.
+template <Dist D>
+int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double divisor, double* out, cudaStream_t s) {
+  const uint64_t inc_hi = (uint64_t)(inc >> 64), inc_lo = (uint64_t)inc;
+  if (D == Dist::Normal) {
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_ki, t.k, sizeof(t.k), 0, cudaMemcpyHostToDevice, s));
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_wi, t.w, sizeof(t.w), 0, cudaMemcpyHostToDevice, s));
+  } else {
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_ke, t.k, sizeof(t.k), 0, cudaMemcpyHostToDevice, s));
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_we, t.w, sizeof(t.w), 0, cudaMemcpyHostToDevice, s));
+  }
     const bool timing = std::getenv("CSC_RNG_TIMING") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -229,7 +242,7 @@ int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
     for (int attempt = 0; attempt < 4; ++attempt, m = m * 2) {
       Scratch raw(sizeof(uint64_t) * m, s), special(m, s);
       const int64_t chunks = (m + kChunk - 1) / kChunk;
-      k_pcg_raw<<<(int)std::min<int64_t>((chunks + 255) / 256, 65535), 256, 0, s>>>(
+      k_pcg_raw<D><<<(int)std::min<int64_t>((chunks + 255) / 256, 65535), 256, 0, s>>>(
           (uint64_t)(s0 >> 64), (uint64_t)s0, inc_hi, inc_lo, m, raw.as<uint64_t>(), special.as<uint8_t>());
       CSC_LAUNCHED();
       // compact the special positions (stable)
@@ -268,14 +281,14 @@ int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
       {
         const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, nspec / 8192));
         std::vector<std::thread> pool;
-        auto work = [&](int t) {
-          for (int64_t q = t; q < nspec; q += nth) {
+        auto work = [&](int th) {
+          for (int64_t q = th; q < nspec; q += nth) {
             HostStream hs{hraw + q * kNear, std::min<int64_t>(kNear, m - hpos[q]), hpos[q], s0, inc};
-            val[q] = slow_draw(hs, tab);
+            val[q] = slow_draw<D>(hs, t);
             cons_all[q] = (int32_t)hs.k;
           }
         };
-        for (int t = 1; t < nth; ++t) pool.emplace_back(work, t);
+        for (int th = 1; th < nth; ++th) pool.emplace_back(work, th);
         work(0);
         for (auto& th : pool) th.join();
       }
@@ -350,20 +363,82 @@ int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
         CSC_CUDA(cudaMemcpyAsync(dsp.get(), sp_pos.data(), sizeof(int64_t) * nsp, cudaMemcpyHostToDevice, s));
         CSC_CUDA(cudaMemcpyAsync(dsv.get(), sp_val.data(), sizeof(double) * nsp, cudaMemcpyHostToDevice, s));
       }
-      k_emit<<<(int)std::min<int64_t>((m + 255) / 256, 65535), 256, 0, s>>>(
+      k_emit<D><<<(int)std::min<int64_t>((m + 255) / 256, 65535), 256, 0, s>>>(
           raw.as<uint64_t>(), special.as<uint8_t>(), is_start.as<uint32_t>(), index.as<uint32_t>(), m, count,
-          dsp.as<int64_t>(), dsv.as<double>(), nsp, divisor, dout.as<double>());
+          dsp.as<int64_t>(), dsv.as<double>(), nsp, divisor, out);
       CSC_LAUNCHED();
-      dout.finish();
       CSC_CUDA(cudaStreamSynchronize(s));
       if (timing)
-        std::fprintf(stderr, "csc_numpy_normals: n=%lld specials=%lld gen %.2f d2h %.2f walk %.2f emit %.2f ms\n",
-                     (long long)count, (long long)nspec, ms(t_start, t_gen), ms(t_gen, t_d2h), ms(t_d2h, t_walk),
+        std::fprintf(stderr, "parity RNG (%s): n=%lld specials=%lld gen %.2f d2h %.2f walk %.2f emit %.2f ms\n",
+                     D == Dist::Normal ? "normal" : "exponential", (long long)count, (long long)nspec, ms(t_start, t_gen), ms(t_gen, t_d2h), ms(t_d2h, t_walk),
                      ms(t_walk, now()));
-      *raw_consumed = end_pos + cons;
+      return end_pos + cons;
+    }
+  fail(CSC_ERR_CUDA, "parity RNG: raw margin exhausted");
+}
+
+Tables tables_of(const Tables& g, const char* what) {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (!g.set) fail(CSC_ERR_INVALID, std::string(what) + " tables not set");
+  return g;
+}
+
+}  // namespace
+
+int64_t numpy_exponentials(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                           double* out, cudaStream_t s) {
+  if (count <= 0) return 0;
+  const Tables t = tables_of(g_exp, "exponential ziggurat");
+  return numpy_draws<Dist::Exponential>(t, make128(state_hi, state_lo), make128(inc_hi, inc_lo), count, 1.0, out, s);
+}
+
+}  // namespace csc
+
+using namespace csc;
+
+extern "C" {
+
+int csc_set_normal_tables(const uint64_t* ki, const double* wi, const double* fi) {
+  return guard([&] {
+    if (!ki || !wi || !fi) fail(CSC_ERR_INVALID, "NULL table");
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    std::memcpy(g_tab.k, ki, sizeof(g_tab.k));
+    std::memcpy(g_tab.w, wi, sizeof(g_tab.w));
+    std::memcpy(g_tab.f, fi, sizeof(g_tab.f));
+    g_tab.set = true;
+  });
+}
+
+int csc_set_exponential_tables(const uint64_t* ke, const double* we, const double* fe) {
+  return guard([&] {
+    if (!ke || !we || !fe) fail(CSC_ERR_INVALID, "NULL table");
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    std::memcpy(g_exp.k, ke, sizeof(g_exp.k));
+    std::memcpy(g_exp.w, we, sizeof(g_exp.w));
+    std::memcpy(g_exp.f, fe, sizeof(g_exp.f));
+    g_exp.set = true;
+  });
+}
+
+int csc_numpy_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                      double divisor, double* out, int64_t* raw_consumed, int device, void* stream) {
+  return guard([&] {
+    if (count < 0) fail(CSC_ERR_INVALID, "count must be >= 0");
+    if (!out && count > 0) fail(CSC_ERR_INVALID, "out is NULL");
+    if (!raw_consumed) fail(CSC_ERR_INVALID, "raw_consumed is NULL");
+    const Tables t = tables_of(g_tab, "normal ziggurat (csc_set_normal_tables)");
+    if (count == 0) {
+      *raw_consumed = 0;
       return;
     }
-    fail(CSC_ERR_CUDA, "parity RNG: raw margin exhausted");
+    DeviceGuard dg(device);
+    ensure_pool(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DeviceOut dout(out, sizeof(double) * count, device, s);
+    *raw_consumed = numpy_draws<Dist::Normal>(t, make128(state_hi, state_lo), make128(inc_hi, inc_lo), count, divisor,
+                                              dout.as<double>(), s);
+    dout.finish();
+    CSC_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -61,13 +61,18 @@ class DeviceGraph:
 
     @classmethod
     def from_edges(cls, src, dst, weights, num_nodes: int, self_loops: str, dtype: int, device: int) -> "DeviceGraph":
-        src = np.ascontiguousarray(src, dtype=np.int64)
-        dst = np.ascontiguousarray(dst, dtype=np.int64)
+        if isinstance(src, np.ndarray) or not hasattr(src, "data_ptr"):
+            src = np.ascontiguousarray(src, dtype=np.int64)
+            dst = np.ascontiguousarray(dst, dtype=np.int64)
+        else:  # CUDA int64 tensors on `device` (edges generated on the GPU)
+            src, dst = src.contiguous(), dst.contiguous()
+            if src.dtype != dst.dtype or str(src.dtype) != "torch.int64" or src.numel() != dst.numel():
+                raise ValueError("device edge arrays must be int64 tensors of equal length")
         w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
         mode = _lib.CSC_SELF_LOOPS_DROP if self_loops == "drop" else _lib.CSC_SELF_LOOPS_ERROR
         out = C.c_void_p()
         _lib.call(
-            "csc_graph_build_coo", int(num_nodes), int(src.size), _lib.ptr(src), _lib.ptr(dst), _lib.ptr(w),
+            "csc_graph_build_coo", int(num_nodes), int(src.shape[0]), _lib.ptr(src), _lib.ptr(dst), _lib.ptr(w),
             mode, dtype, device, _lib.current_stream(device), C.byref(out),
         )
         nnz = C.c_int64(0)

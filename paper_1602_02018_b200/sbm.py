@@ -12,6 +12,7 @@ asks for, which the reference does not have.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass
 from typing import Sequence
@@ -27,6 +28,7 @@ __all__ = [
     "critical_epsilon",
     "dcsbm_generate",
     "sbm_edges",
+    "sbm_edges_device",
     "sbm_generate",
 ]
 
@@ -136,9 +138,71 @@ def _device_build(src, dst, num_nodes: int, device: int | None) -> Graph:
     return graph
 
 
+def _sbm_pairs(cfg: SbmConfig):
+    """Per community pair (a <= b, the reference's loop order, sbm.py:133-145) the
+    quantities of _success_positions: cells, q and the batch size, for the pairs that
+    contribute (cells > 0, q > 0); ``search`` is set when one of them has q >= 1/3."""
+    sizes = np.asarray(cfg.sizes, dtype=np.int64)
+    first = np.concatenate([[0], np.cumsum(sizes)])
+    a, b = np.triu_indices(cfg.k)
+    diag = a == b
+    cells = np.where(diag, sizes[a] * (sizes[a] - 1) // 2, sizes[a] * sizes[b])
+    q = np.where(diag, cfg.q1, cfg.q2)
+    live = (cells > 0) & (q > 0.0)  # pairs that contribute edges (q >= 1: all cells, no draws)
+    search = bool(np.any(live & (q >= 1.0 / 3.0)))
+    a, b, diag, cells, q = a[live], b[live], diag[live], cells[live], q[live]
+    mean = q * cells.astype(np.float64)
+    batch = np.maximum(64, (mean + 10.0 * np.sqrt(mean) + 10.0).astype(np.int64))
+    return a, b, diag, cells, q, batch, first, sizes, search
+
+
+def sbm_edges_device(cfg: SbmConfig, device: int | None = None):
+    """``sbm_edges`` on the device (csc_sbm_edges): the same edges in the same order as
+    int64 CUDA tensors, plus the labels; ``None`` when a pair probability is >= 1/3
+    (numpy's search branch, left to the host) or numpy's tables are unavailable."""
+    import torch
+
+    from ._npzig import exponential_tables, pcg_state
+
+    dev = _lib.default_device() if device is None else int(device)
+    a, b, diag, cells, q, batch, first, sizes, search = _sbm_pairs(cfg)
+    labels = np.repeat(np.arange(cfg.k), sizes)
+    if search:
+        return None
+    try:
+        ke, we, fe = exponential_tables()
+    except RuntimeError:
+        return None
+    _lib.call("csc_set_exponential_tables", _lib.ptr(ke), _lib.ptr(we), _lib.ptr(fe))
+    st, inc = pcg_state(np.random.default_rng(cfg.seed))
+    l1mq = np.array([math.log1p(-float(x)) for x in (cfg.q1, cfg.q2)])[np.where(diag, 0, 1)]
+    cap = int(batch.sum())
+    tdev = torch.device("cuda", dev)
+    src = torch.empty(max(cap, 1), dtype=torch.int64, device=tdev)
+    dst = torch.empty(max(cap, 1), dtype=torch.int64, device=tdev)
+    n_e, raws = C.c_int64(0), C.c_int64(0)
+    m = _MASK64
+    pairs = [np.ascontiguousarray(x) for x in (cells.astype(np.int64), l1mq, batch.astype(np.int64),
+                                               diag.astype(np.int32), first[a].astype(np.int64),
+                                               first[b].astype(np.int64), sizes[b].astype(np.int64))]
+    _lib.call("csc_sbm_edges", st >> 64, st & m, inc >> 64, inc & m, int(a.size), *[_lib.ptr(x) for x in pairs],
+              cap, src.data_ptr(), dst.data_ptr(), C.byref(n_e), C.byref(raws), dev, _lib.current_stream(dev))
+    return src[: n_e.value], dst[: n_e.value], labels
+
+
+_MASK64 = (1 << 64) - 1
+
+
 def sbm_generate(cfg: SbmConfig, *, device: int | None = None) -> tuple[Graph, np.ndarray]:
-    """SBM graph (unit weights, nodes ordered by community) and its labels (reference sbm.py:118-155)."""
-    src, dst, labels = sbm_edges(cfg)
+    """SBM graph (unit weights, nodes ordered by community) and its labels (reference sbm.py:118-155).
+
+    The edges are drawn on the device when every pair probability is below 1/3
+    (``sbm_edges_device``; bit-identical to the host restatement ``sbm_edges``)."""
+    out = sbm_edges_device(cfg, device)
+    if out is None:
+        src, dst, labels = sbm_edges(cfg)
+    else:
+        src, dst, labels = out
     return _device_build(src, dst, cfg.num_nodes, device), labels
 
 
