@@ -1,6 +1,8 @@
 // Gather microbenchmark: random 64-byte row gathers from an L2-sized panel.
 //   A: LDG.128 per lane (4 lanes per row), 4 gathers in flight per lane (the K2 scheme)
 //   B: TMA tile::gather4 into shared memory, mbarrier completion, 1 issuing lane per row
+//   C: cp.async (LDGSTS.128, L2-only) into a per-warp ring of STAGES chunk buffers
+//      (8 rows x 4 neighbours x 64 B = 2 KB each): in-flight depth set by shared memory
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_bench gather_bench.cu -lcuda
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -91,6 +93,55 @@ __global__ void __launch_bounds__(128) k_tma(const __grid_constant__ CUtensorMap
   }
 }
 
+// C: work item = (row batch of 8, chunk of 4 neighbours); items of a warp are pipelined
+template <int STAGES>
+__global__ void __launch_bounds__(256) k_cpasync(const float* __restrict__ G, const int* __restrict__ idx, int n,
+                                                  float* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane & 3, grp = lane >> 2;
+  unsigned char* ring = smem + (size_t)wid * STAGES * 2048;
+  const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+  const long nbatch = (n + 7) / 8;
+  const long mybatches = warp < nbatch ? (nbatch - warp + nw - 1) / nw : 0;
+  const long items = mybatches * (DEG / 4);
+  auto issue = [&](long it) {
+    if (it < items) {
+      const long b = warp + (it / (DEG / 4)) * nw;
+      const int e = (int)(it % (DEG / 4));
+      const long row = b * 8 + grp;
+      const int st = (int)(it % STAGES);
+      const uint32_t base = (uint32_t)__cvta_generic_to_shared(ring + st * 2048 + grp * 256 + sub * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = row < n ? idx[row * DEG + e * 4 + k] : 0;
+        const float* src = G + (size_t)j * PW + sub * 4;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(base + k * 64), "l"(src) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int k = 0; k < STAGES - 1; ++k) issue(k);
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (long it = 0; it < items; ++it) {
+    issue(it + STAGES - 1);
+    asm volatile("cp.async.wait_group %0;" :: "n"(STAGES - 1) : "memory");
+    __syncwarp();
+    const float4* buf = reinterpret_cast<const float4*>(ring + (it % STAGES) * 2048 + grp * 256);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 v = buf[k * 4 + sub];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if ((it % (DEG / 4)) == DEG / 4 - 1) {
+      const long row = (warp + (it / (DEG / 4)) * nw) * 8 + grp;
+      if (row < n) reinterpret_cast<float4*>(out + row * PW)[sub] = acc;
+      acc = make_float4(0, 0, 0, 0);
+    }
+    __syncwarp();
+  }
+}
+
 int main() {
   const int n = 1000000;
   std::vector<int> h(n * (size_t)DEG);
@@ -148,6 +199,32 @@ int main() {
   CK(cudaMemcpy(got.data(), out, sizeof(float) * got.size(), cudaMemcpyDeviceToHost));
   double maxd = 0; for (size_t i = 0; i < got.size(); ++i) maxd = fmax(maxd, fabs(got[i] - ref[i]));
   printf("TMA vs LDG max abs diff %.3g\n", maxd);
+  auto run_cp = [&](auto kern, int stages, bool timed) {
+    size_t smem = (size_t)8 * stages * 2048;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+    kern<<<sms * occ, 256, smem>>>(G, idx, n, out);
+    CK(cudaGetLastError());
+    if (!timed) return 0.f;
+    cudaEventRecord(e0);
+    for (int it = 0; it < 10; ++it) kern<<<sms * occ, 256, smem>>>(G, idx, n, out);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("  (cp.async stages=%d: %d CTAs/SM = %d warps, %zu KB in flight/SM)\n", stages, occ, occ * 8,
+           (size_t)occ * smem / 1024);
+    return ms / 10;
+  };
+  CK(cudaMemset(out, 0, sizeof(float) * n * PW));
+  run_cp(k_cpasync<3>, 3, false); CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(got.data(), out, sizeof(float) * got.size(), cudaMemcpyDeviceToHost));
+  maxd = 0; for (size_t i = 0; i < got.size(); ++i) maxd = fmax(maxd, fabs(got[i] - ref[i]));
+  printf("cp.async vs LDG max abs diff %.3g\n", maxd);
+  report("cp.async stages=2", run_cp(k_cpasync<2>, 2, true));
+  report("cp.async stages=3", run_cp(k_cpasync<3>, 3, true));
+  report("cp.async stages=4", run_cp(k_cpasync<4>, 4, true));
+  report("cp.async stages=6", run_cp(k_cpasync<6>, 6, true));
+  report("cp.async stages=8", run_cp(k_cpasync<8>, 8, true));
   report("TMA gather4 stages=2 bps=2", run_tma(k_tma<2>, 2, 2, true));
   report("TMA gather4 stages=3 bps=1", run_tma(k_tma<3>, 3, 1, true));
   report("TMA gather4 stages=3 bps=2", run_tma(k_tma<3>, 3, 2, true));
