@@ -408,6 +408,7 @@ static int launch_epi(const StepArgs& a, int lpr, int threads, int device, cudaS
     if (unit) return launch_lpr<T, EPI, 4, 8, true>(a, lpr, threads, device, s);
     return launch_lpr<T, EPI, 4, 8, false>(a, lpr, threads, device, s);
   }
+
   if (unit) return launch_lpr<T, EPI, 4, 6, true>(a, lpr, threads, device, s);
   return launch_lpr<T, EPI, 4, 6, false>(a, lpr, threads, device, s);
 }
@@ -635,19 +636,26 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
     while (pw < forced && pw < max_pw) pw *= 2;
     max_pw = pw;
   } else {
-    // widest power-of-two panel whose gather source fits the L2 budget.  Low-degree
-    // graphs re-read each gathered row fewer times, so L2 misses cost less than the
-    // extra CSR pass of another panel: the budget grows as 16 / mean degree (<= 4x).
+    // Gathers cost per L2 request more than per byte (64-B rows run at ~2/3 the speed of
+    // 128-B rows per request), and every panel re-reads the CSR, so: panel rows of at
+    // least 128 B; wider when the panel still fits the L2 budget (which grows as
+    // 16 / mean degree, <= 4x: low-degree graphs re-read gathered rows less often); and
+    // the whole block in one panel when its rows are <= 256 B.  Measured on B200 at
+    // BASELINE C2-C5, fp32 and fp64 (profiles/r01_panel_sweeps.txt): 10-23 % faster than
+    // L2-fit-only panels at C3/C5, equal where the block is L2-resident.
     const double deg = n > 0 ? (double)nnz / (double)n : 16.0;
     const double relax = std::min(4.0, std::max(1.0, 16.0 / std::max(deg, 1.0)));
     const double budget =
         relax * (double)device_props(device).l2_bytes * (double)g_opt.l2_budget_pct.load() / 100.0;
-    int pw = vec;
-    while (pw * 2 <= max_pw && (double)n * (pw * 2) * dtype_size(dtype) <= budget) pw *= 2;
-    // nothing fits: 8 lanes per row (32 fp32 / 16 fp64 columns) -- wider rows per lane
-    // group lose more than the CSR passes they save (measured at N = 16e6, d = 67)
-    if ((double)n * pw * dtype_size(dtype) > budget) pw = 8 * vec;
-    max_pw = pw;
+    int pw_l2 = vec;
+    while (pw_l2 * 2 <= max_pw && (double)n * (pw_l2 * 2) * dtype_size(dtype) <= budget) pw_l2 *= 2;
+    int pw = std::max(pw_l2, 128 / (int)dtype_size(dtype));
+    if ((size_t)w * dtype_size(dtype) <= 256) {
+      int one = vec;
+      while (one < w) one *= 2;
+      pw = std::max(pw, one);
+    }
+    max_pw = std::min(pw, max_pw);
   }
   PanelPlan pp;
   int c0 = 0;
