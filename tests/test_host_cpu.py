@@ -194,3 +194,56 @@ def test_numpy_ziggurat_restatement():
     assert np.array_equal(got, rng.standard_normal(50_000))
     assert (ns.s, ns.inc) == Z.pcg_state(rng)
     assert ns.raw_count > 50_000  # slow paths consumed extra raws
+
+
+def test_numpy_geometric_restatement():
+    """numpy's geometric (exponential ziggurat / inversion, and the search branch) restated draw for draw."""
+    from paper_1602_02018_b200 import _npzig as Z
+
+    tabs = Z.ziggurat_tables(), Z.exponential_tables()
+    for p in (2e-5, 1e-3, 0.3, 0.5):
+        rng = np.random.default_rng(7)
+        ns = Z.NormalStream(*Z.pcg_state(rng), *tabs)
+        got = [ns.geometric(p) for _ in range(4000)]
+        assert np.array_equal(got, rng.geometric(p, size=4000)), p
+        assert (ns.s, ns.inc) == Z.pcg_state(rng)
+
+
+def test_sbm_pair_table_matches_reference_loop():
+    """The per-pair table handed to csc_sbm_edges follows _success_positions' batch rule and pair order."""
+    import math
+
+    from paper_1602_02018_b200.sbm import SbmConfig, _sbm_pairs
+
+    cfg = SbmConfig(num_nodes=2003, k=7, avg_degree=9, epsilon=0.05, seed=1)
+    a, b, diag, cells, q, batch, first, sizes, search = _sbm_pairs(cfg)
+    assert not search
+    exp = []
+    for i in range(cfg.k):
+        for j in range(i, cfg.k):
+            c = cfg.sizes[i] * (cfg.sizes[i] - 1) // 2 if i == j else cfg.sizes[i] * cfg.sizes[j]
+            qq = cfg.q1 if i == j else cfg.q2
+            if c > 0 and qq > 0:
+                mean = qq * c
+                exp.append((i, j, c, max(64, int(mean + 10.0 * math.sqrt(mean) + 10.0))))
+    assert [(int(x), int(y), int(c), int(bb)) for x, y, c, bb in zip(a, b, cells, batch)] == exp
+
+
+def test_new_abi_argument_validation():
+    """csc_kmeans_replicates / csc_sbm_edges reject bad arguments before touching a device."""
+    pts = np.zeros((3, 2))
+    lab = np.empty((1, 3), dtype=np.int64)
+    inert, its = np.empty(1), np.empty(1, dtype=np.int64)
+    with pytest.raises(ValueError, match="at least k"):
+        _lib.call("csc_kmeans_replicates", _lib.ptr(pts), 3, 2, 5, 1, None, None, _lib.ptr(np.zeros((1, 5, 2))), 10,
+                  1e-6, _lib.ptr(lab), None, _lib.ptr(inert), _lib.ptr(its), None, 0, None)
+    with pytest.raises(ValueError, match="seeding states or initial centroids"):
+        _lib.call("csc_kmeans_replicates", _lib.ptr(pts), 3, 2, 2, 1, None, None, None, 10, 1e-6, _lib.ptr(lab),
+                  None, _lib.ptr(inert), _lib.ptr(its), None, 0, None)
+    one = lambda v, dt: np.array([v], dtype=dt)  # noqa: E731
+    n_e = np.zeros(1, dtype=np.int64)
+    args = [one(100, np.int64), one(np.log1p(-0.5), np.float64), one(64, np.int64), one(1, np.int32),
+            one(0, np.int64), one(0, np.int64), one(15, np.int64)]
+    with pytest.raises(ValueError, match="1/3"):
+        _lib.call("csc_sbm_edges", 1, 2, 3, 5, 1, *[_lib.ptr(x) for x in args], 0, None, None, _lib.ptr(n_e), None,
+                  0, None)
