@@ -123,32 +123,39 @@ def device_normal_block(rng: np.random.Generator, n: int, w: int, device: int = 
 
 
 class DeviceProbeStream:
-    """Sequential probe blocks drawn on the GPU (same values as ProbeStream), one block
-    ahead: a worker thread draws block t + 1 on its own CUDA stream (kernels + the host
-    walk of the rare slow paths) while the caller filters block t."""
+    """Sequential probe blocks drawn on the GPU (same values as ProbeStream), ``depth``
+    blocks ahead: a worker thread draws blocks t + 1 .. t + depth in order on its own
+    CUDA stream (kernels + the host walk of the rare slow paths) while the caller
+    filters block t.  A draw takes about as long as a probe's filter, so one block of
+    lookahead stalls whenever a draw runs late; the generator is private to the caller
+    (run_csc's "probe" substream), so drawing blocks that end up unused changes nothing."""
 
-    def __init__(self, rng: np.random.Generator, n: int, ds: int, device: int):
+    def __init__(self, rng: np.random.Generator, n: int, ds: int, device: int, depth: int = 2):
         import torch
 
         self.rng, self.n, self.ds, self.device = rng, n, ds, device
+        self.depth = max(1, int(depth))
         self.side = torch.cuda.Stream(device=device)
-        self.bufs = [torch.empty((n, ds), dtype=torch.float64, device=f"cuda:{device}") for _ in range(2)]
+        self.bufs = [torch.empty((n, ds), dtype=torch.float64, device=f"cuda:{device}")
+                     for _ in range(self.depth + 1)]
         self.i = 0
         self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="csc-probe-devrng")
-        self.next = self.pool.submit(self._draw, 0)
+        self.pending = [self.pool.submit(self._draw, k) for k in range(self.depth)]
 
     def _draw(self, slot: int):
         return device_normal_block(self.rng, self.n, self.ds, self.device, self.bufs[slot], self.side)
 
     def take(self):
-        block = self.next.result()  # drawn and synchronised on the side stream
+        block = self.pending.pop(0).result()  # drawn and synchronised on the side stream
+        # the slot of block i - 1 is free again: the caller's use of it has finished
+        # (eigencount returns after a sync)
+        self.pending.append(self.pool.submit(self._draw, (self.i + self.depth) % (self.depth + 1)))
         self.i += 1
-        # the caller's use of the previous block has finished (eigencount returns after a sync)
-        self.next = self.pool.submit(self._draw, self.i % 2)
         return block
 
     def close(self) -> None:
         try:
-            self.next.result()
+            for f in self.pending:
+                f.result()
         finally:
             self.pool.shutdown(wait=True)

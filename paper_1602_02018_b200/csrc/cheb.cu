@@ -352,7 +352,9 @@ static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t
   }
   const int64_t rows_per_block = (int64_t)(threads / 32) * (32 / LPR);
   int64_t need = (a.n + rows_per_block - 1) / rows_per_block;
-  const int64_t cap = std::min<int64_t>((int64_t)device_props(device).sms * occ, step_grid_cap(device));
+  const int64_t cap = g_opt.persistent.load() ? std::min<int64_t>((int64_t)device_props(device).sms * occ,
+                                                                    step_grid_cap(device))
+                                              : (int64_t)INT32_MAX;
   const int grid = (int)std::max<int64_t>(1, std::min(need, cap));
   const size_t persist = a.G ? persist_bytes(device) : 0;
   if (persist > 0) {

@@ -73,6 +73,7 @@ struct Options {
   std::atomic<int64_t> unroll{4};         // neighbour gathers in flight per lane (4 or 8)
   std::atomic<int64_t> row_order{0};      // 0 interleaved row groups, 1 contiguous ranges per warp
   std::atomic<int64_t> l2_persist_pct{0}; // >0: keep the gathered panel in a persisting L2 window
+  std::atomic<int64_t> persistent{1};     // 1: step grid = resident CTAs (grid-stride); 0: one CTA per row block
 };
 extern Options g_opt;
 
@@ -115,14 +116,20 @@ class Scratch {
  public:
   Scratch() = default;
   Scratch(size_t bytes, cudaStream_t s) { alloc(bytes, s); }
+  // from a specific memory pool (e.g. side_pool: work on a side stream that must not
+  // share freed blocks -- and thereby stream dependencies -- with the filter's scratch)
+  Scratch(size_t bytes, cudaStream_t s, cudaMemPool_t pool) { alloc(bytes, s, pool); }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
   ~Scratch() { release(); }
-  void alloc(size_t bytes, cudaStream_t s) {
+  void alloc(size_t bytes, cudaStream_t s, cudaMemPool_t pool = nullptr) {
     release();
     s_ = s;
     if (bytes == 0) bytes = 16;
-    CSC_CUDA(cudaMallocAsync(&p_, bytes, s));
+    if (pool)
+      CSC_CUDA(cudaMallocFromPoolAsync(&p_, bytes, pool, s));
+    else
+      CSC_CUDA(cudaMallocAsync(&p_, bytes, s));
     bytes_ = bytes;
   }
   void release() {
@@ -146,6 +153,10 @@ class Scratch {
 // device memory; returns the raw uint64 consumed.
 int64_t numpy_exponentials(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
                            double* out, cudaStream_t s);
+
+// A second stream-ordered pool per device (never trimmed) for work that runs on a
+// side stream concurrently with filters (the parity RNG's scratch).
+cudaMemPool_t side_pool(int dev);
 
 // Host or device?  Device pointers must belong to `device`.
 bool is_device_ptr(const void* p, int device);

@@ -227,6 +227,9 @@ T* pinned_buffer(size_t count, int slot) {
 template <Dist D>
 int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double divisor, double* out, cudaStream_t s) {
   const uint64_t inc_hi = (uint64_t)(inc >> 64), inc_lo = (uint64_t)inc;
+  int dev = 0;
+  CSC_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t mp = side_pool(dev);
   if (D == Dist::Normal) {
     CSC_CUDA(cudaMemcpyToSymbolAsync(c_ki, t.k, sizeof(t.k), 0, cudaMemcpyHostToDevice, s));
     CSC_CUDA(cudaMemcpyToSymbolAsync(c_wi, t.w, sizeof(t.w), 0, cudaMemcpyHostToDevice, s));
@@ -240,18 +243,18 @@ int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double di
     auto t_start = now();
     int64_t m = count + count / 16 + 4096;  // ~2.2 % of raws are consumed inside slow paths
     for (int attempt = 0; attempt < 4; ++attempt, m = m * 2) {
-      Scratch raw(sizeof(uint64_t) * m, s), special(m, s);
+      Scratch raw(sizeof(uint64_t) * m, s, mp), special(m, s, mp);
       const int64_t chunks = (m + kChunk - 1) / kChunk;
       k_pcg_raw<D><<<(int)std::min<int64_t>((chunks + 255) / 256, 65535), 256, 0, s>>>(
           (uint64_t)(s0 >> 64), (uint64_t)s0, inc_hi, inc_lo, m, raw.as<uint64_t>(), special.as<uint8_t>());
       CSC_LAUNCHED();
       // compact the special positions (stable)
-      Scratch pos(sizeof(int64_t) * m, s), nsel(sizeof(int64_t), s);
+      Scratch pos(sizeof(int64_t) * m, s, mp), nsel(sizeof(int64_t), s, mp);
       size_t tb = 0;
       thrust::counting_iterator<int64_t> it(0);
       CSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, special.as<uint8_t>(), pos.as<int64_t>(),
                                           nsel.as<int64_t>(), m, s));
-      Scratch tmp(tb, s);
+      Scratch tmp(tb, s, mp);
       CSC_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, special.as<uint8_t>(), pos.as<int64_t>(),
                                           nsel.as<int64_t>(), m, s));
       CSC_LAUNCHED();
@@ -264,7 +267,7 @@ int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double di
       // raws following each special position (slow paths read a few more)
       constexpr int kNear = 8;
       uint64_t* hraw = pinned_buffer<uint64_t>((size_t)nspec * kNear, 1);
-      Scratch gath(sizeof(uint64_t) * std::max<int64_t>(nspec * kNear, 1), s);
+      Scratch gath(sizeof(uint64_t) * std::max<int64_t>(nspec * kNear, 1), s, mp);
       if (nspec) {
         k_gather_near<<<(int)std::min<int64_t>((nspec * kNear + 255) / 256, 65535), 256, 0, s>>>(
             raw.as<uint64_t>(), pos.as<int64_t>(), nspec, m, kNear, gath.as<uint64_t>());
@@ -340,11 +343,11 @@ int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double di
         if (itb != skip_begin.end() && *itb == end_pos + 1) cons = 1 + skip_len[itb - skip_begin.begin()];
       }
       // device: mask skipped positions, number the starts, emit
-      Scratch is_start(sizeof(uint32_t) * m, s), index(sizeof(uint32_t) * m, s);
+      Scratch is_start(sizeof(uint32_t) * m, s, mp), index(sizeof(uint32_t) * m, s, mp);
       k_init_starts<<<(int)std::min<int64_t>((m + 255) / 256, 65535), 256, 0, s>>>(m, is_start.as<uint32_t>());
       CSC_LAUNCHED();
       const int64_t nskip = (int64_t)skip_begin.size();
-      Scratch dsb(sizeof(int64_t) * std::max<int64_t>(nskip, 1), s), dsl(sizeof(int32_t) * std::max<int64_t>(nskip, 1), s);
+      Scratch dsb(sizeof(int64_t) * std::max<int64_t>(nskip, 1), s, mp), dsl(sizeof(int32_t) * std::max<int64_t>(nskip, 1), s, mp);
       if (nskip) {
         CSC_CUDA(cudaMemcpyAsync(dsb.get(), skip_begin.data(), sizeof(int64_t) * nskip, cudaMemcpyHostToDevice, s));
         CSC_CUDA(cudaMemcpyAsync(dsl.get(), skip_len.data(), sizeof(int32_t) * nskip, cudaMemcpyHostToDevice, s));
@@ -354,11 +357,11 @@ int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double di
       }
       size_t tb2 = 0;
       CSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
-      Scratch tmp2(tb2, s);
+      Scratch tmp2(tb2, s, mp);
       CSC_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.get(), tb2, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
       CSC_LAUNCHED();
       const int64_t nsp = (int64_t)sp_pos.size();
-      Scratch dsp(sizeof(int64_t) * std::max<int64_t>(nsp, 1), s), dsv(sizeof(double) * std::max<int64_t>(nsp, 1), s);
+      Scratch dsp(sizeof(int64_t) * std::max<int64_t>(nsp, 1), s, mp), dsv(sizeof(double) * std::max<int64_t>(nsp, 1), s, mp);
       if (nsp) {
         CSC_CUDA(cudaMemcpyAsync(dsp.get(), sp_pos.data(), sizeof(int64_t) * nsp, cudaMemcpyHostToDevice, s));
         CSC_CUDA(cudaMemcpyAsync(dsv.get(), sp_val.data(), sizeof(double) * nsp, cudaMemcpyHostToDevice, s));

@@ -109,6 +109,22 @@ void ensure_pool(int dev) {
   g_pool_done[dev] = true;
 }
 
+cudaMemPool_t side_pool(int dev) {
+  static cudaMemPool_t pools[64] = {};
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (dev < 0 || dev >= 64) fail(CSC_ERR_INVALID, "device index out of range");
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CSC_CUDA(cudaMemPoolCreate(&pools[dev], &props));
+    uint64_t threshold = UINT64_MAX;
+    CSC_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &threshold));
+  }
+  return pools[dev];
+}
+
 bool is_device_ptr(const void* p, int device) {
   cudaPointerAttributes a;
   cudaError_t e = cudaPointerGetAttributes(&a, p);
@@ -153,6 +169,7 @@ static std::atomic<int64_t>* option_slot(const char* key) {
   if (k == "l2_budget_pct") return &g_opt.l2_budget_pct;
   if (k == "unroll") return &g_opt.unroll;
   if (k == "l2_persist_pct") return &g_opt.l2_persist_pct;
+  if (k == "persistent") return &g_opt.persistent;
   if (k == "row_order") return &g_opt.row_order;
   return nullptr;
 }
@@ -168,6 +185,7 @@ int csc_set_option(const char* key, int64_t value) {
     if (k == "panel_width" && value < 0) fail(CSC_ERR_INVALID, "panel_width must be >= 0");
     if (k == "unroll" && value != 2 && value != 4 && value != 8) fail(CSC_ERR_INVALID, "unroll must be 2, 4 or 8");
     if (k == "l2_persist_pct" && (value < 0 || value > 100)) fail(CSC_ERR_INVALID, "l2_persist_pct in [0, 100]");
+    if (k == "persistent" && value != 0 && value != 1) fail(CSC_ERR_INVALID, "persistent must be 0 or 1");
     if (k == "l2_budget_pct" && (value < 1 || value > 100)) fail(CSC_ERR_INVALID, "l2_budget_pct in [1, 100]");
     slot->store(value);
   });
