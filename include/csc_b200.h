@@ -55,6 +55,8 @@ typedef struct csc_graph csc_graph;
 typedef struct csc_comm csc_comm; /* NCCL communicator for row-sharded operators */
 
 #define CSC_UNIQUE_ID_BYTES 128
+typedef struct csc_peers csc_peers; /* peer-memory transport for row-sharded operators */
+#define CSC_PEER_HANDLE_BYTES 64
 
 /* ---- library ------------------------------------------------------------ */
 int csc_abi_version(void);
@@ -269,6 +271,26 @@ int csc_graph_create_rows(int64_t num_nodes, int64_t row_begin, int64_t num_rows
 int csc_cheb_filter_rows(const csc_graph* g, csc_comm* comm, const double* coeffs, int ncoeffs, const void* X,
                          int64_t ldx, void* Y, int64_t ldy, int ncols, int io_dtype, int mode, double* out,
                          void* stream);
+
+/* Peer-memory transport (the all-gather fused into the step kernel over NVLink):
+ * csc_peers_create allocates this rank's two gather panels of panel_bytes each
+ * (>= R * nranks * csc_panel_row_bytes(...)) plus a flag array, exportable by
+ * CUDA IPC; csc_peers_handle writes its CSC_PEER_HANDLE_BYTES handle; every rank
+ * distributes its handle (e.g. torch.distributed all_gather_object) and calls
+ * csc_peers_attach for every other rank.  A one-rank transport is ready at once. */
+int csc_panel_row_bytes(int64_t num_nodes, int ncols, int dtype, int device, int64_t nnz, int64_t* out);
+int csc_peers_create(int nranks, int rank, int device, size_t panel_bytes, csc_peers** out);
+int csc_peers_handle(const csc_peers* peers, uint8_t* out /* CSC_PEER_HANDLE_BYTES */);
+int csc_peers_attach(csc_peers* peers, int peer_rank, const uint8_t* handle);
+int csc_peers_destroy(csc_peers* peers);
+
+/* csc_cheb_filter_rows over the peer transport: each mid step's epilogue stores
+ * this rank's finished rows into every rank's next gather panel (ping-pong) and
+ * a system-scope flag barrier separates steps -- no collective call.  Same modes
+ * and results as csc_cheb_filter_rows. */
+int csc_cheb_filter_rows_peers(const csc_graph* g, csc_peers* peers, const double* coeffs, int ncoeffs,
+                               const void* X, int64_t ldx, void* Y, int64_t ldy, int ncols, int io_dtype, int mode,
+                               double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -272,6 +272,13 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
         // default write-back: this panel is the next step's gather source, let it stay in L2
         *reinterpret_cast<V*>(O + off) = VT::make(out);
       }
+      if constexpr (EPI == EPI_NONE) {  // (peer stores happen on mid steps only)
+      if (a.npeers > 0) {  // fused all-gather: this row into every rank's next gather panel
+        const size_t poff = (size_t)(a.peer_row0 + row) * PW + col0;
+        for (int q = 0; q < a.npeers; ++q)
+          *reinterpret_cast<V*>(static_cast<T*>(a.peers[q]) + poff) = VT::make(out);
+      }
+      }
       if constexpr (EPI == EPI_SUMSQ || EPI == EPI_ROWSQ) {
 #pragma unroll
         for (int c = 0; c < VEC; ++c)

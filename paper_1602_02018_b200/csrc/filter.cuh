@@ -68,6 +68,12 @@ struct StepArgs {
   int last;      // symmetric-basis output + isolated-node fixup (+ epilogue)
   int hints;     // evict-first hints on streamed operands (set by launch_step)
   int contig;    // contiguous row ranges per warp (set by launch_step)
+  // row-sharded peer transport (rows.cu): O's rows are also stored into every rank's next
+  // gather panel, peers[q] + (peer_row0 + row) * pw, over NVLink -- the all-gather fused
+  // into the step.  npeers = 0: off.
+  void* const* peers;  // device array of npeers panel pointers
+  int npeers;
+  int64_t peer_row0;
 };
 
 struct PanelPlan {

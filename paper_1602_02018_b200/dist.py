@@ -340,15 +340,34 @@ def local_csr(graph, begin: int, end: int):
     return indptr, np.ascontiguousarray(graph.indices[lo:hi], dtype=np.int32), np.ascontiguousarray(graph.weights[lo:hi])
 
 
-class RowShardedOperator:
-    """This rank's rows of the normalized Laplacian plus an NCCL communicator.
+def exchange_handles(grp: Group, handle: np.ndarray) -> list[np.ndarray]:
+    """Every rank's CUDA IPC handle bytes, in rank order (all_gather over the group)."""
+    import torch.distributed as dist
 
-    Blocks are passed as this rank's rows (CUDA tensors, N_local x w).
+    got: list = [None] * grp.world
+    dist.all_gather_object(got, bytes(np.asarray(handle, dtype=np.uint8)), group=grp.group)
+    return [np.frombuffer(b, dtype=np.uint8).copy() for b in got]
+
+
+class RowShardedOperator:
+    """This rank's rows of the normalized Laplacian plus the step exchange.
+
+    Blocks are passed as this rank's rows (CUDA tensors, N_local x w).  ``transport``:
+    ``"nccl"`` -- an ncclAllGather of every step's rows (csc_cheb_filter_rows);
+    ``"peer"`` -- the all-gather fused into the step kernel: rows are stored straight
+    into every rank's CUDA-IPC-mapped gather panel over NVLink, with a flag barrier
+    between steps (csc_cheb_filter_rows_peers).  Both give the same results.
     """
 
-    def __init__(self, graph, grp: Group, dtype: str = "float32", device: int | None = None):
+    def __init__(self, graph, grp: Group, dtype: str = "float32", device: int | None = None,
+                 transport: str = "nccl"):
         import torch
 
+        if transport not in ("nccl", "peer"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
+        self.peers = None
+        self._peer_bytes = 0
         self.grp = grp
         self.num_nodes = graph.num_nodes
         self.device = _lib.default_device() if device is None else int(device)
@@ -360,6 +379,10 @@ class RowShardedOperator:
                   _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(weights), _lib.dtype_code(dtype), self.device,
                   _lib.current_stream(self.device), C.byref(h))
         self.handle = h.value
+        self.local_nnz = int(indices.size)
+        self.comm = None
+        if transport == "peer":
+            return
         uid = np.zeros(128, dtype=np.uint8)
         if grp.rank == 0:
             _lib.call("csc_comm_unique_id", _lib.ptr(uid))
@@ -387,10 +410,42 @@ class RowShardedOperator:
             out = np.zeros(1)
         elif mode == 2:
             out = torch.empty(X.shape[0], dtype=torch.float64, device=X.device)
-        _lib.call("csc_cheb_filter_rows", self.handle, self.comm, _lib.ptr(c), int(c.size), X.data_ptr(),
+        if self.transport == "peer":
+            self._ensure_peers(int(X.shape[1]))
+            fn, tr = "csc_cheb_filter_rows_peers", self.peers
+        else:
+            fn, tr = "csc_cheb_filter_rows", self.comm
+        _lib.call(fn, self.handle, tr, _lib.ptr(c), int(c.size), X.data_ptr(),
                   int(X.stride(0)), None if Y is None else Y.data_ptr(), int(X.shape[1]), int(X.shape[1]),
                   _lib.dtype_code(X.dtype), mode, _lib.ptr(out), _lib.current_stream(self.device))
         return Y, out
+
+    def _ensure_peers(self, ncols: int) -> None:
+        """(Re)build the peer transport when this block needs wider panels (collective)."""
+        row_bytes = C.c_int64(0)
+        _lib.call("csc_panel_row_bytes", self.num_nodes, ncols, _lib.dtype_code(self.dtype), self.device,
+                  self.local_nnz * self.grp.world, C.byref(row_bytes))
+        rows = -(-self.num_nodes // self.grp.world) * self.grp.world
+        need = rows * int(row_bytes.value)
+        if self.peers is not None and need <= self._peer_bytes:
+            return
+        self._close_peers()
+        pe = C.c_void_p()
+        _lib.call("csc_peers_create", self.grp.world, self.grp.rank, self.device, need, C.byref(pe))
+        self.peers, self._peer_bytes = pe.value, need
+        if self.grp.world > 1:
+            handle = np.zeros(64, dtype=np.uint8)
+            _lib.call("csc_peers_handle", self.peers, _lib.ptr(handle))
+            handles = exchange_handles(self.grp, handle)
+            for r, hb in enumerate(handles):
+                if r != self.grp.rank:
+                    _lib.call("csc_peers_attach", self.peers, r, _lib.ptr(hb))
+
+    def _close_peers(self) -> None:
+        lib = _lib._lib
+        if self.peers and lib is not None:
+            lib.csc_peers_destroy(self.peers)
+        self.peers, self._peer_bytes = None, 0
 
     def apply_filter(self, filt: PolyFilter, X_local):
         """h(L) X for this rank's rows."""
@@ -419,6 +474,8 @@ class RowShardedOperator:
         lib = _lib._lib
         if lib is None:
             return
+        if getattr(self, "peers", None):
+            self._close_peers()
         if getattr(self, "comm", None):
             lib.csc_comm_destroy(self.comm)
             self.comm = None

@@ -211,3 +211,15 @@ def test_row_sharded_recurrence_matches_oracle():
     for b, e, out in parts:
         got[b:e] = out
     assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def _exchange(grp):
+    handle = np.full(64, 10 + grp.rank, dtype=np.uint8)
+    return [h.tolist() for h in D.exchange_handles(grp, handle)]
+
+
+def test_peer_handle_exchange_rank_order():
+    """The peer transport's IPC handle exchange returns every rank's handle in rank order."""
+    got = run_world(_exchange)
+    for per_rank in got:
+        assert per_rank == [[10] * 64, [11] * 64]

@@ -124,13 +124,15 @@ def test_dcsbm_run_csc_vs_oracle():
     assert P.adjusted_rand_index(r.labels, o["labels"]) >= 0.99
 
 
-def test_row_sharded_single_rank_matches_replicated():
-    """Row-sharded operator (NCCL all-gather after every step) with one rank == the replicated path."""
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_row_sharded_single_rank_matches_replicated(transport):
+    """Row-sharded operator (NCCL all-gather after every step, or peer stores fused into the
+    step kernel) with one rank == the replicated path."""
     import torch
 
     g = c1_op().graph
     for dtype, tol in (("float64", 1e-12), ("float32", 1e-5)):
-        rop = D.RowShardedOperator(g, D.Group(0, 1), dtype=dtype)
+        rop = D.RowShardedOperator(g, D.Group(0, 1), dtype=dtype, transport=transport)
         op = P.laplacian_op(g, dtype=dtype)
         X = np.random.default_rng(2).standard_normal((1000, 21))
         filt = P.design_lowpass(0.45, 50)
@@ -145,3 +147,26 @@ def test_row_sharded_single_rank_matches_replicated():
         fref = P.build_features(op, filt, P.features.RandomSignals(X, "gaussian", None))
         assert relerr(F.double().cpu().numpy(), fref.rows) <= tol
         assert np.array_equal(zero, fref.zero_rows)
+
+
+def test_row_sharded_peer_transport_bit_equal_to_nccl():
+    """The fused peer-store transport moves the same values as the NCCL all-gather: results are
+    bit-identical for every recurrence branch (orders 0-3 and 50), several panels per block and
+    repeated calls (epochs advance; the transport grows for wider blocks)."""
+    import torch
+
+    g = c1_op().graph
+    for dtype in ("float64", "float32"):
+        tdt = torch.float64 if dtype == "float64" else torch.float32
+        a = D.RowShardedOperator(g, D.Group(0, 1), dtype=dtype, transport="nccl")
+        b = D.RowShardedOperator(g, D.Group(0, 1), dtype=dtype, transport="peer")
+        for w in (5, 100, 7):
+            X = torch.tensor(np.random.default_rng(w).standard_normal((1000, w)), dtype=tdt, device="cuda")
+            for order in (0, 1, 2, 3, 50):
+                filt = P.design_lowpass(0.6, order) if order else P.PolyFilter(np.array([0.7]), 0.6, 0, "none", "lowpass")
+                ya, yb = a.apply_filter(filt, X), b.apply_filter(filt, X)
+                assert torch.equal(ya, yb), (dtype, w, order)
+            assert a.eigencount(filt, X) == b.eigencount(filt, X)
+            fa, za = a.features(filt, X)
+            fb, zb = b.features(filt, X)
+            assert torch.equal(fa, fb) and np.array_equal(za, zb)
