@@ -6,13 +6,15 @@
 //   1. device: PCG64 raw outputs u_i (128-bit LCG jump-ahead per thread chunk,
 //      XSL-RR output); a raw is "special" if, as the start of a draw, it fails
 //      the ziggurat's fast test (rabs >= ki[layer]) -- ~1 % of positions;
-//   2. host: a sequential walk over the special positions decides which are
-//      draw starts and evaluates their wedge / tail paths with the C library's
-//      exp / log1p (the functions numpy's own C code calls), recording each
-//      start's value and how many raws it consumed;
-//   3. device: positions consumed inside slow paths are masked, a scan numbers
-//      the remaining starts, fast draws are +-rabs * wi[layer], and every value
-//      is divided by `divisor` into the output.
+//   2. device: every special is evaluated as if it started a draw (wedge tests
+//      with numpy's operation order; CUDA's exp decides only comparisons that
+//      clear an 8-ulp margin); draws reaching a tail (their value needs libm's
+//      log1p) or a closer call are evaluated on the host with the C library's
+//      exp / log1p -- the functions numpy's own C code calls -- in one round trip;
+//   3. device: which specials start a draw (a prefix max of the positions their
+//      slow paths reach; short sequential walks inside clusters), positions
+//      consumed inside slow paths are masked, a scan numbers the starts, fast
+//      draws are +-rabs * wi[layer], and every value is divided by `divisor`.
 // The caller advances its numpy generator by the returned raw count, so later
 // host draws continue the same stream.
 #include <cub/cub.cuh>
@@ -24,7 +26,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
-#include <thread>
 #include <vector>
 
 #include "internal.cuh"
@@ -44,6 +45,8 @@ __constant__ uint64_t c_ki[256];  // normal:      ki / wi
 __constant__ double c_wi[256];
 __constant__ uint64_t c_ke[256];  // exponential: ke / we
 __constant__ double c_we[256];
+__constant__ double c_fi[256];    // wedge tables (slow paths on the device)
+__constant__ double c_fe[256];
 
 struct Tables {
   uint64_t k[256];
@@ -93,16 +96,6 @@ __global__ void k_pcg_raw(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t 
       special[i] = is_special<D>(u) ? 1 : 0;
     }
   }
-}
-
-// positions consumed inside slow paths are not draw starts
-__global__ void k_mark_skips(const int64_t* __restrict__ skip_begin, const int32_t* __restrict__ skip_len, int64_t nskip,
-                             int64_t m, uint32_t* __restrict__ is_start) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nskip; t += (int64_t)gridDim.x * blockDim.x)
-    for (int k = 0; k < skip_len[t]; ++k) {
-      const int64_t p = skip_begin[t] + k;
-      if (p < m) is_start[p] = 0;
-    }
 }
 
 __global__ void k_gather_near(const uint64_t* __restrict__ raw, const int64_t* __restrict__ pos, int64_t nspec,
@@ -221,162 +214,300 @@ T* pinned_buffer(size_t count, int slot) {
   return static_cast<T*>(buf[slot]);
 }
 
+// raw output at stream position i (from the generated buffer, else by jump-ahead)
+__device__ inline uint64_t raw_at(const uint64_t* __restrict__ raw, int64_t m, int64_t i, u128 s0, u128 inc) {
+  if (i < m) return raw[i];
+  u128 st = pcg_advance(s0, inc, (uint64_t)i);
+  return pcg_next(st, inc);
+}
+
+__device__ inline double raw_double(uint64_t u) { return (double)(u >> 11) * (1.0 / 9007199254740992.0); }
+
+// The wedge test compares against libm's exp in the reference; CUDA's exp is within
+// 1 ulp and glibc's within ~0.5 ulp of the true value, so a comparison that clears
+// 8 ulp is decided identically.  Closer calls go to the host.
+__device__ inline bool too_close(double lhs, double rhs) {
+  return fabs(lhs - rhs) <= 8.0 * 2.220446049250313e-16 * fabs(rhs);
+}
+
+// Every special position evaluated as if it started a draw (numpy's slow paths, same
+// operation order as the C code: no FMA contraction): value and raws consumed; draws
+// that reach a tail (libm log1p) or a too-close wedge test are flagged for the host.
+template <Dist D>
+__global__ void k_slow_eval(const uint64_t* __restrict__ raw, int64_t m, const int64_t* __restrict__ pos,
+                            int64_t nspec, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo,
+                            double* __restrict__ val, int32_t* __restrict__ cons, uint8_t* __restrict__ flag) {
+  const u128 s0 = make128(s_hi, s_lo), inc = make128(i_hi, i_lo);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nspec; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pos[q];
+    int k = 0;
+    bool host = true;
+    double v = 0.0;
+    for (int tries = 0; tries < 32; ++tries) {
+      const uint64_t u = raw_at(raw, m, p + k, s0, inc);
+      ++k;
+      double x, lhs, rhs;
+      if (D == Dist::Normal) {
+        const int idx = (int)(u & 0xff);
+        const uint64_t r = u >> 8;
+        const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+        x = (double)rabs * c_wi[idx];
+        if (r & 1) x = -x;
+        if (rabs < c_ki[idx]) { v = x; host = false; break; }
+        if (idx == 0) break;  // tail: libm log1p decides value and consumption
+        const double uu = raw_double(raw_at(raw, m, p + k, s0, inc));
+        ++k;
+        lhs = __dadd_rn(__dmul_rn(__dsub_rn(c_fi[idx - 1], c_fi[idx]), uu), c_fi[idx]);
+        rhs = exp(__dmul_rn(__dmul_rn(-0.5, x), x));
+      } else {
+        uint64_t ri = u >> 3;
+        const int idx = (int)(ri & 0xff);
+        ri >>= 8;
+        x = (double)ri * c_we[idx];
+        if (ri < c_ke[idx]) { v = x; host = false; break; }
+        if (idx == 0) break;  // tail: ziggurat_exp_r - log1p(-u)
+        const double uu = raw_double(raw_at(raw, m, p + k, s0, inc));
+        ++k;
+        lhs = __dadd_rn(__dmul_rn(__dsub_rn(c_fe[idx - 1], c_fe[idx]), uu), c_fe[idx]);
+        rhs = exp(-x);
+      }
+      if (too_close(lhs, rhs)) break;
+      if (lhs < rhs) { v = x; host = false; break; }
+      // rejected: numpy retries the whole draw from the next raw
+    }
+    val[q] = v;
+    cons[q] = k;
+    flag[q] = host ? 1 : 0;
+  }
+}
+
+__global__ void k_flag_pos(const int64_t* __restrict__ pos, const int64_t* __restrict__ fidx,
+                           const int64_t* __restrict__ nfl_p, int64_t* __restrict__ fpos) {
+  const int64_t nfl = *nfl_p;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nfl; t += (int64_t)gridDim.x * blockDim.x)
+    fpos[t] = pos[fidx[t]];
+}
+
+__global__ void k_scatter_host(const int64_t* __restrict__ fidx, int64_t nfl, const double* __restrict__ hv,
+                               const int32_t* __restrict__ hc, double* __restrict__ val, int32_t* __restrict__ cons) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nfl; t += (int64_t)gridDim.x * blockDim.x) {
+    val[fidx[t]] = hv[t];
+    cons[fidx[t]] = hc[t];
+  }
+}
+
+__global__ void k_reach(const int64_t* __restrict__ pos, const int32_t* __restrict__ cons, int64_t nspec,
+                        int64_t* __restrict__ reach) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nspec; q += (int64_t)gridDim.x * blockDim.x)
+    reach[q] = pos[q] + cons[q];
+}
+
+// Which specials start a draw: a special that no earlier special's slow path reaches
+// (prefix max of reach <= its position) heads a cluster and starts a draw; inside a
+// cluster the starts follow sequentially (clusters are a few specials long).
+__global__ void k_resolve(const int64_t* __restrict__ pos, const int32_t* __restrict__ cons,
+                          const int64_t* __restrict__ pmax, int64_t nspec, uint8_t* __restrict__ start) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nspec; q += (int64_t)gridDim.x * blockDim.x) {
+    if (pmax[q] > pos[q]) continue;  // not a cluster head
+    start[q] = 1;
+    int64_t next_free = pos[q] + cons[q];
+    for (int64_t r = q + 1; r < nspec && pmax[r] > pos[r]; ++r) {
+      if (pos[r] >= next_free) {
+        start[r] = 1;
+        next_free = pos[r] + cons[r];
+      } else {
+        start[r] = 0;
+      }
+    }
+  }
+}
+
+// positions consumed inside a starting special's slow path are not draw starts;
+// covered specials are not starts either
+__global__ void k_mark_consumed(const int64_t* __restrict__ pos, const int32_t* __restrict__ cons,
+                                const uint8_t* __restrict__ start, int64_t nspec, int64_t m,
+                                uint32_t* __restrict__ is_start) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nspec; q += (int64_t)gridDim.x * blockDim.x) {
+    if (!start[q]) {
+      is_start[pos[q]] = 0;
+      continue;
+    }
+    for (int j = 1; j < cons[q]; ++j)
+      if (pos[q] + j < m) is_start[pos[q] + j] = 0;
+  }
+}
+
+// the count-th draw: its position and the raws it consumed
+__global__ void k_find_end(const uint32_t* __restrict__ is_start, const uint32_t* __restrict__ index, int64_t m,
+                           int64_t count, const uint8_t* __restrict__ special, const int64_t* __restrict__ pos,
+                           const int32_t* __restrict__ cons, int64_t nspec, int64_t* __restrict__ end) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!is_start[i] || (int64_t)index[i] != count - 1) continue;
+    int64_t c = 1;
+    if (special[i]) {
+      int64_t lo = 0, hi = nspec;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pos[mid] < i) lo = mid + 1;
+        else hi = mid;
+      }
+      c = cons[lo];
+    }
+    end[0] = i;
+    end[1] = c;
+  }
+}
+
+inline int grid_of(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 65535)); }
+
 // The first `count` draws of numpy's Generator(PCG64) stream of distribution D
 // from state (s0, inc), divided by `divisor`, into device memory; returns the
-// number of raw uint64 the draws consumed.
+// number of raw uint64 the draws consumed.  Everything runs on the device except
+// the few slow paths k_slow_eval flags (one host round trip).
 template <Dist D>
 int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double divisor, double* out, cudaStream_t s) {
   const uint64_t inc_hi = (uint64_t)(inc >> 64), inc_lo = (uint64_t)inc;
+  const uint64_t s_hi = (uint64_t)(s0 >> 64), s_lo = (uint64_t)s0;
   int dev = 0;
   CSC_CUDA(cudaGetDevice(&dev));
   cudaMemPool_t mp = side_pool(dev);
   if (D == Dist::Normal) {
     CSC_CUDA(cudaMemcpyToSymbolAsync(c_ki, t.k, sizeof(t.k), 0, cudaMemcpyHostToDevice, s));
     CSC_CUDA(cudaMemcpyToSymbolAsync(c_wi, t.w, sizeof(t.w), 0, cudaMemcpyHostToDevice, s));
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_fi, t.f, sizeof(t.f), 0, cudaMemcpyHostToDevice, s));
   } else {
     CSC_CUDA(cudaMemcpyToSymbolAsync(c_ke, t.k, sizeof(t.k), 0, cudaMemcpyHostToDevice, s));
     CSC_CUDA(cudaMemcpyToSymbolAsync(c_we, t.w, sizeof(t.w), 0, cudaMemcpyHostToDevice, s));
+    CSC_CUDA(cudaMemcpyToSymbolAsync(c_fe, t.f, sizeof(t.f), 0, cudaMemcpyHostToDevice, s));
   }
-    const bool timing = std::getenv("CSC_RNG_TIMING") != nullptr;
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    auto t_start = now();
-    int64_t m = count + count / 16 + 4096;  // ~2.2 % of raws are consumed inside slow paths
-    for (int attempt = 0; attempt < 4; ++attempt, m = m * 2) {
-      Scratch raw(sizeof(uint64_t) * m, s, mp), special(m, s, mp);
-      const int64_t chunks = (m + kChunk - 1) / kChunk;
-      k_pcg_raw<D><<<(int)std::min<int64_t>((chunks + 255) / 256, 65535), 256, 0, s>>>(
-          (uint64_t)(s0 >> 64), (uint64_t)s0, inc_hi, inc_lo, m, raw.as<uint64_t>(), special.as<uint8_t>());
-      CSC_LAUNCHED();
-      // compact the special positions (stable)
-      Scratch pos(sizeof(int64_t) * m, s, mp), nsel(sizeof(int64_t), s, mp);
+  const bool timing = std::getenv("CSC_RNG_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  auto t_start = now();
+  int64_t m = count + count / 16 + 4096;  // ~2 % of raws are consumed inside slow paths
+  for (int attempt = 0; attempt < 4; ++attempt, m = m * 2) {
+    // 1. raws + special flags; compact the special positions (stable)
+    Scratch raw(sizeof(uint64_t) * m, s, mp), special(m, s, mp);
+    const int64_t chunks = (m + kChunk - 1) / kChunk;
+    k_pcg_raw<D><<<(int)std::min<int64_t>((chunks + 255) / 256, 65535), 256, 0, s>>>(
+        s_hi, s_lo, inc_hi, inc_lo, m, raw.as<uint64_t>(), special.as<uint8_t>());
+    CSC_LAUNCHED();
+    Scratch pos(sizeof(int64_t) * m, s, mp), nsel(2 * sizeof(int64_t), s, mp);
+    thrust::counting_iterator<int64_t> it(0);
+    {
       size_t tb = 0;
-      thrust::counting_iterator<int64_t> it(0);
       CSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, special.as<uint8_t>(), pos.as<int64_t>(),
                                           nsel.as<int64_t>(), m, s));
       Scratch tmp(tb, s, mp);
       CSC_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, special.as<uint8_t>(), pos.as<int64_t>(),
                                           nsel.as<int64_t>(), m, s));
       CSC_LAUNCHED();
-      int64_t nspec = 0;
-      CSC_CUDA(cudaMemcpyAsync(&nspec, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    }
+    int64_t nspec = 0;
+    CSC_CUDA(cudaMemcpyAsync(&nspec, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CSC_CUDA(cudaStreamSynchronize(s));
+    // 2. slow paths on the device
+    const int64_t ns1 = std::max<int64_t>(nspec, 1);
+    Scratch val(sizeof(double) * ns1, s, mp), cons(sizeof(int32_t) * ns1, s, mp), flag(ns1, s, mp),
+        fidx(sizeof(int64_t) * ns1, s, mp);
+    int64_t nfl = 0;
+    if (nspec > 0) {
+      k_slow_eval<D><<<grid_of(nspec), 256, 0, s>>>(raw.as<uint64_t>(), m, pos.as<int64_t>(), nspec, s_hi, s_lo,
+                                                    inc_hi, inc_lo, val.as<double>(), cons.as<int32_t>(),
+                                                    flag.as<uint8_t>());
+      CSC_LAUNCHED();
+      size_t tb = 0;
+      CSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag.as<uint8_t>(), fidx.as<int64_t>(),
+                                          nsel.as<int64_t>() + 1, nspec, s));
+      Scratch tmp(tb, s, mp);
+      CSC_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, flag.as<uint8_t>(), fidx.as<int64_t>(),
+                                          nsel.as<int64_t>() + 1, nspec, s));
+      CSC_LAUNCHED();
+      CSC_CUDA(cudaMemcpyAsync(&nfl, nsel.as<int64_t>() + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       CSC_CUDA(cudaStreamSynchronize(s));
+    }
+    {
       auto t_gen = now();
-      int64_t* hpos = pinned_buffer<int64_t>(nspec, 0);
-      if (nspec) CSC_CUDA(cudaMemcpyAsync(hpos, pos.get(), sizeof(int64_t) * nspec, cudaMemcpyDeviceToHost, s));
-      // raws following each special position (slow paths read a few more)
-      constexpr int kNear = 8;
-      uint64_t* hraw = pinned_buffer<uint64_t>((size_t)nspec * kNear, 1);
-      Scratch gath(sizeof(uint64_t) * std::max<int64_t>(nspec * kNear, 1), s, mp);
-      if (nspec) {
-        k_gather_near<<<(int)std::min<int64_t>((nspec * kNear + 255) / 256, 65535), 256, 0, s>>>(
-            raw.as<uint64_t>(), pos.as<int64_t>(), nspec, m, kNear, gath.as<uint64_t>());
+      // 3. flagged slow paths on the host (libm), results scattered back
+      if (nfl > 0) {
+        constexpr int kNear = 8;
+        Scratch fpos(sizeof(int64_t) * nfl, s, mp), gath(sizeof(uint64_t) * nfl * kNear, s, mp);
+        k_flag_pos<<<grid_of(nfl), 256, 0, s>>>(pos.as<int64_t>(), fidx.as<int64_t>(), nsel.as<int64_t>() + 1,
+                                                fpos.as<int64_t>());
         CSC_LAUNCHED();
-        CSC_CUDA(cudaMemcpyAsync(hraw, gath.get(), sizeof(uint64_t) * nspec * kNear, cudaMemcpyDeviceToHost, s));
-      }
-      CSC_CUDA(cudaStreamSynchronize(s));
-      auto t_d2h = now();
-      // every special evaluated as if it started a draw (its value and consumption
-      // depend only on its own raws): in parallel host threads with the C library's
-      // exp / log1p, then a sequential pass keeps the real starts
-      std::vector<double> val(nspec);
-      std::vector<int32_t> cons_all(nspec);
-      {
-        const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, nspec / 8192));
-        std::vector<std::thread> pool;
-        auto work = [&](int th) {
-          for (int64_t q = th; q < nspec; q += nth) {
-            HostStream hs{hraw + q * kNear, std::min<int64_t>(kNear, m - hpos[q]), hpos[q], s0, inc};
-            val[q] = slow_draw<D>(hs, t);
-            cons_all[q] = (int32_t)hs.k;
-          }
-        };
-        for (int th = 1; th < nth; ++th) pool.emplace_back(work, th);
-        work(0);
-        for (auto& th : pool) th.join();
-      }
-      std::vector<int64_t> sp_pos, skip_begin;
-      std::vector<double> sp_val;
-      std::vector<int32_t> skip_len;
-      int64_t next_free = 0, skipped = 0;
-      for (int64_t q = 0; q < nspec; ++q) {
-        const int64_t p = hpos[q];
-        if (p < next_free) continue;      // consumed by an earlier slow path
-        if (p - skipped >= count) break;  // draws before p already complete the request
-        sp_pos.push_back(p);
-        sp_val.push_back(val[q]);
-        if (cons_all[q] > 1) {
-          skip_begin.push_back(p + 1);
-          skip_len.push_back(cons_all[q] - 1);
-          skipped += cons_all[q] - 1;
+        k_gather_near<<<grid_of(nfl * kNear), 256, 0, s>>>(raw.as<uint64_t>(), fpos.as<int64_t>(), nfl, m, kNear,
+                                                          gath.as<uint64_t>());
+        CSC_LAUNCHED();
+        int64_t* hpos = pinned_buffer<int64_t>(nfl, 0);
+        uint64_t* hraw = pinned_buffer<uint64_t>((size_t)nfl * kNear, 1);
+        double* hv = pinned_buffer<double>(nfl, 2);
+        int32_t* hc = pinned_buffer<int32_t>(nfl, 3);
+        CSC_CUDA(cudaMemcpyAsync(hpos, fpos.get(), sizeof(int64_t) * nfl, cudaMemcpyDeviceToHost, s));
+        CSC_CUDA(cudaMemcpyAsync(hraw, gath.get(), sizeof(uint64_t) * nfl * kNear, cudaMemcpyDeviceToHost, s));
+        CSC_CUDA(cudaStreamSynchronize(s));
+        for (int64_t q = 0; q < nfl; ++q) {
+          HostStream hs{hraw + q * kNear, std::min<int64_t>(kNear, m - hpos[q]), hpos[q], s0, inc};
+          hv[q] = slow_draw<D>(hs, t);
+          hc[q] = (int32_t)hs.k;
         }
-        next_free = p + cons_all[q];
+        Scratch dv(sizeof(double) * nfl, s, mp), dc(sizeof(int32_t) * nfl, s, mp);
+        CSC_CUDA(cudaMemcpyAsync(dv.get(), hv, sizeof(double) * nfl, cudaMemcpyHostToDevice, s));
+        CSC_CUDA(cudaMemcpyAsync(dc.get(), hc, sizeof(int32_t) * nfl, cudaMemcpyHostToDevice, s));
+        k_scatter_host<<<grid_of(nfl), 256, 0, s>>>(fidx.as<int64_t>(), nfl, dv.as<double>(), dc.as<int32_t>(),
+                                                   val.as<double>(), cons.as<int32_t>());
+        CSC_LAUNCHED();
+        CSC_CUDA(cudaStreamSynchronize(s));  // pinned staging is reused by the next call
       }
-      auto t_walk = now();
-      // position of the count-th draw start
-      // starts are all positions not inside a skip run; the j-th start (0-based) is at
-      // j + (skipped raws before it).  Walk the skip runs to locate start `count - 1`.
-      int64_t before = 0;  // skipped raws before the current position
-      int64_t end_pos = -1;
-      {
-        int64_t target = count - 1;  // draw index
-        size_t r = 0;
-        int64_t cur = 0;  // candidate position = target + before
-        for (;;) {
-          cur = target + before;
-          if (r < skip_begin.size() && skip_begin[r] <= cur) {
-            before += skip_len[r];
-            ++r;
-            continue;
-          }
-          break;
-        }
-        end_pos = cur;
-      }
-      if (end_pos >= m) continue;  // not enough raws generated: retry with more
-      // consumption of the last draw
-      int64_t cons = 1;
-      auto itp = std::lower_bound(sp_pos.begin(), sp_pos.end(), end_pos);
-      if (itp != sp_pos.end() && *itp == end_pos) {
-        // its consumption is recorded in the skip run that follows it (if any)
-        auto itb = std::lower_bound(skip_begin.begin(), skip_begin.end(), end_pos + 1);
-        if (itb != skip_begin.end() && *itb == end_pos + 1) cons = 1 + skip_len[itb - skip_begin.begin()];
-      }
-      // device: mask skipped positions, number the starts, emit
-      Scratch is_start(sizeof(uint32_t) * m, s, mp), index(sizeof(uint32_t) * m, s, mp);
-      k_init_starts<<<(int)std::min<int64_t>((m + 255) / 256, 65535), 256, 0, s>>>(m, is_start.as<uint32_t>());
+      auto t_eval = now();
+      // 4. which specials start a draw; mask consumed positions; number the starts
+      Scratch reach(sizeof(int64_t) * std::max<int64_t>(nspec, 1), s, mp),
+          pmax(sizeof(int64_t) * std::max<int64_t>(nspec, 1), s, mp), start(std::max<int64_t>(nspec, 1), s, mp);
+      Scratch is_start(sizeof(uint32_t) * m, s, mp), index(sizeof(uint32_t) * m, s, mp), end(2 * sizeof(int64_t), s, mp);
+      k_init_starts<<<grid_of(m), 256, 0, s>>>(m, is_start.as<uint32_t>());
       CSC_LAUNCHED();
-      const int64_t nskip = (int64_t)skip_begin.size();
-      Scratch dsb(sizeof(int64_t) * std::max<int64_t>(nskip, 1), s, mp), dsl(sizeof(int32_t) * std::max<int64_t>(nskip, 1), s, mp);
-      if (nskip) {
-        CSC_CUDA(cudaMemcpyAsync(dsb.get(), skip_begin.data(), sizeof(int64_t) * nskip, cudaMemcpyHostToDevice, s));
-        CSC_CUDA(cudaMemcpyAsync(dsl.get(), skip_len.data(), sizeof(int32_t) * nskip, cudaMemcpyHostToDevice, s));
-        k_mark_skips<<<(int)std::min<int64_t>((nskip + 255) / 256, 65535), 256, 0, s>>>(
-            dsb.as<int64_t>(), dsl.as<int32_t>(), nskip, m, is_start.as<uint32_t>());
+      if (nspec > 0) {
+        k_reach<<<grid_of(nspec), 256, 0, s>>>(pos.as<int64_t>(), cons.as<int32_t>(), nspec, reach.as<int64_t>());
+        CSC_LAUNCHED();
+        size_t tb2 = 0;
+        CSC_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tb2, reach.as<int64_t>(), pmax.as<int64_t>(), cub::Max(),
+                                                (int64_t)-1, nspec, s));
+        Scratch tmp2(tb2, s, mp);
+        CSC_CUDA(cub::DeviceScan::ExclusiveScan(tmp2.get(), tb2, reach.as<int64_t>(), pmax.as<int64_t>(), cub::Max(),
+                                                (int64_t)-1, nspec, s));
+        CSC_LAUNCHED();
+        k_resolve<<<grid_of(nspec), 256, 0, s>>>(pos.as<int64_t>(), cons.as<int32_t>(), pmax.as<int64_t>(), nspec,
+                                                start.as<uint8_t>());
+        CSC_LAUNCHED();
+        k_mark_consumed<<<grid_of(nspec), 256, 0, s>>>(pos.as<int64_t>(), cons.as<int32_t>(), start.as<uint8_t>(),
+                                                      nspec, m, is_start.as<uint32_t>());
         CSC_LAUNCHED();
       }
-      size_t tb2 = 0;
-      CSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
-      Scratch tmp2(tb2, s, mp);
-      CSC_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.get(), tb2, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
+      size_t tb3 = 0;
+      CSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb3, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
+      Scratch tmp3(tb3, s, mp);
+      CSC_CUDA(cub::DeviceScan::ExclusiveSum(tmp3.get(), tb3, is_start.as<uint32_t>(), index.as<uint32_t>(), m, s));
       CSC_LAUNCHED();
-      const int64_t nsp = (int64_t)sp_pos.size();
-      Scratch dsp(sizeof(int64_t) * std::max<int64_t>(nsp, 1), s, mp), dsv(sizeof(double) * std::max<int64_t>(nsp, 1), s, mp);
-      if (nsp) {
-        CSC_CUDA(cudaMemcpyAsync(dsp.get(), sp_pos.data(), sizeof(int64_t) * nsp, cudaMemcpyHostToDevice, s));
-        CSC_CUDA(cudaMemcpyAsync(dsv.get(), sp_val.data(), sizeof(double) * nsp, cudaMemcpyHostToDevice, s));
-      }
-      k_emit<D><<<(int)std::min<int64_t>((m + 255) / 256, 65535), 256, 0, s>>>(
-          raw.as<uint64_t>(), special.as<uint8_t>(), is_start.as<uint32_t>(), index.as<uint32_t>(), m, count,
-          dsp.as<int64_t>(), dsv.as<double>(), nsp, divisor, out);
+      CSC_CUDA(cudaMemsetAsync(end.get(), 0xff, 2 * sizeof(int64_t), s));
+      k_find_end<<<grid_of(m), 256, 0, s>>>(is_start.as<uint32_t>(), index.as<uint32_t>(), m, count,
+                                            special.as<uint8_t>(), pos.as<int64_t>(), cons.as<int32_t>(), nspec,
+                                            end.as<int64_t>());
       CSC_LAUNCHED();
+      // 5. emit (the values of special starts come from val)
+      k_emit<D><<<grid_of(m), 256, 0, s>>>(raw.as<uint64_t>(), special.as<uint8_t>(), is_start.as<uint32_t>(),
+                                           index.as<uint32_t>(), m, count, pos.as<int64_t>(), val.as<double>(), nspec,
+                                           divisor, out);
+      CSC_LAUNCHED();
+      int64_t hend[2] = {-1, -1};
+      CSC_CUDA(cudaMemcpyAsync(hend, end.get(), sizeof(hend), cudaMemcpyDeviceToHost, s));
       CSC_CUDA(cudaStreamSynchronize(s));
       if (timing)
-        std::fprintf(stderr, "parity RNG (%s): n=%lld specials=%lld gen %.2f d2h %.2f walk %.2f emit %.2f ms\n",
-                     D == Dist::Normal ? "normal" : "exponential", (long long)count, (long long)nspec, ms(t_start, t_gen), ms(t_gen, t_d2h), ms(t_d2h, t_walk),
-                     ms(t_walk, now()));
-      return end_pos + cons;
+        std::fprintf(stderr, "parity RNG (%s): n=%lld specials=%lld host=%lld gen %.2f eval %.2f emit %.2f ms\n",
+                     D == Dist::Normal ? "normal" : "exponential", (long long)count, (long long)nspec,
+                     (long long)nfl, ms(t_start, t_gen), ms(t_gen, t_eval), ms(t_eval, now()));
+      if (hend[0] < 0) continue;  // fewer than `count` starts in the generated raws: retry with more
+      return hend[0] + hend[1];
     }
+  }
   fail(CSC_ERR_CUDA, "parity RNG: raw margin exhausted");
 }
 
