@@ -325,7 +325,11 @@ def run_ours(args, cfg):
     if rank != 0:
         return
     peak, peak_src = peaks()
-    achieved = step_bytes / (step_ms / 1e3) / 1e9 if step_ms > 0 else None
+    # SURVEY.md 8(d) unit: one fused Chebyshev step on the N x d block moves B_step(d) =
+    # B_csr + 5 N d s algorithmic bytes (B_first for the first step), whatever recurrence
+    # the kernel uses; achieved = those bytes of the timed filters / the K2 launches' time
+    alg_per_step_set = work  # B_first + (p - 1) B_step per filter, one filter per step
+    achieved = alg_per_step_set * args.steps / (step_ms / 1e3) / 1e9 if step_ms > 0 else None
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
@@ -335,7 +339,10 @@ def run_ours(args, cfg):
         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
         "kernel": "k_cheb_step (fused Chebyshev step SpMM)", "peak_source": peak_src,
         "kernel_ms_per_launch": step_ms / max(step_launches, 1), "launches_timed": step_launches,
-        "algorithmic_bytes_per_launch": step_bytes / max(step_launches, 1),
+        "algorithmic_bytes_per_launch": alg_per_step_set * args.steps / max(step_launches, 1),
+        "algorithmic_unit": "SURVEY.md 8(d) B_step(d) = B_csr + 5 N d s per step launch (B_first on the first); "
+                            "one launch per step when the block is one panel",
+        "kernel_stream_bytes_per_launch": step_bytes / max(step_launches, 1),
         "kernel_share_of_step": (step_ms / args.steps) / ms if ms > 0 else None,
         "recurrence": "clenshaw" if _lib.get_option("recurrence") == 0 else "forward",
         # K2 is bound by the neighbour-gather traffic through L2 (deg x row bytes per step), not by
