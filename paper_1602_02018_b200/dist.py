@@ -26,7 +26,6 @@ exchange logic with the gloo backend.
 from __future__ import annotations
 
 import ctypes as C
-import math
 import time
 from dataclasses import dataclass
 
