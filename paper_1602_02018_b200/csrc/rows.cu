@@ -219,8 +219,12 @@ __global__ void k_peer_barrier(void* const* flag_ptrs, int nranks, int rank, uin
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
   const uint64_t* mine = static_cast<const uint64_t*>(flag_ptrs[rank]) + q;
   uint64_t v = 0;
+  const long long t0 = clock64();
   do {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    // a peer that never arrives (died, or called with a different block) would hang the
+    // GPU: after ~1 minute of cycles fail the launch instead
+    if (v < epoch && clock64() - t0 > 120000000000ll) __trap();
   } while (v < epoch);
 }
 
