@@ -94,10 +94,17 @@ __device__ double sq_row(const double* x, int d) {
   return pw_sum([x](int64_t t) { return __dmul_rn(x[t], x[t]); }, 0, d);
 }
 
-// ((a - b) ** 2).sum() of one row
-__device__ double sqdiff_row(const double* a, const double* b, int d) {
-  return pw_sum([a, b](int64_t t) {
-    const double u = __dsub_rn(a[t], b[t]);
+// the same on column j of a transposed (d x k) centroid block
+__device__ double sq_col(const double* C, int64_t k, int j, int d) {
+  return pw_sum([C, k, j](int64_t t) {
+    const double x = C[t * k + j];
+    return __dmul_rn(x, x);
+  }, 0, d);
+}
+
+__device__ double sqdiff_col(const double* a, const double* C, int64_t k, int j, int d) {
+  return pw_sum([a, C, k, j](int64_t t) {
+    const double u = __dsub_rn(a[t], C[t * k + j]);
     return __dmul_rn(u, u);
   }, 0, d);
 }
@@ -107,7 +114,15 @@ __global__ void k_sqnorm(const double* __restrict__ X, int64_t rows, int d, doub
     out[i] = sq_row(X + i * d, d);
 }
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 1024;
+
+// Byte offsets of the per-replicate arrays in dynamic shared memory (-1: global slice).
+// The seeding walks near/cdf sequentially in one thread and Lloyd scans lab per
+// cluster, so those go to shared memory first, then the centroids.
+struct SmemPlan {
+  int64_t near = -1, cdf = -1, lab = -1, C = -1;
+  size_t bytes = 0;
+};
 
 struct RepScratch {
   double* C;      // k x d centroids (global slice, used when they do not fit in shared memory)
@@ -120,18 +135,20 @@ struct RepScratch {
 __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
     const double* __restrict__ P, const double* __restrict__ pp, int64_t n, int d, int k, const int64_t* first,
     const uint64_t* pcg, const double* init, int64_t max_iters, double tol, double* Cg, double* near_g, double* cdf_g,
-    int* lab_g, int* mem_g, int c_in_smem, int64_t* labels_out, double* centroids_out, double* inertia_out,
+    int* lab_g, int* mem_g, SmemPlan sp, int64_t* labels_out, double* centroids_out, double* inertia_out,
     int64_t* iters_out, int* status_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int r = blockIdx.x, tid = threadIdx.x;
   double* cc = reinterpret_cast<double*>(smem_raw);  // k
   int* counts = reinterpret_cast<int*>(cc + k);      // k
   int* offs = counts + k;                            // k
-  double* C = c_in_smem ? reinterpret_cast<double*>(smem_raw + (((size_t)k * 16 + 15) / 16) * 16)
-                        : Cg + (int64_t)r * k * d;
-  double* near = near_g + (int64_t)r * n;
-  double* cdf = cdf_g + (int64_t)r * n;
-  int* lab = lab_g + (int64_t)r * n;
+  // per-warp copy of the point being assigned (read once per point, not once per centroid chunk)
+  double* pbuf = reinterpret_cast<double*>(smem_raw + (((size_t)k * 16 + 15) / 16) * 16);
+  // centroids stored transposed (d x k): conflict-free shared-memory reads in the assignment
+  double* C = sp.C >= 0 ? reinterpret_cast<double*>(smem_raw + sp.C) : Cg + (int64_t)r * k * d;
+  double* near = sp.near >= 0 ? reinterpret_cast<double*>(smem_raw + sp.near) : near_g + (int64_t)r * n;
+  double* cdf = sp.cdf >= 0 ? reinterpret_cast<double*>(smem_raw + sp.cdf) : cdf_g + (int64_t)r * n;
+  int* lab = sp.lab >= 0 ? reinterpret_cast<int*>(smem_raw + sp.lab) : lab_g + (int64_t)r * n;
   int* members = mem_g + (int64_t)r * n;
   __shared__ int64_t s_pick;
   __shared__ double s_inertia;
@@ -146,9 +163,9 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
       inc = make128(pcg[4 * r + 2], pcg[4 * r + 3]);
     }
     const double* p0 = P + first[r] * d;
-    for (int t = tid; t < d; t += kThreads) C[t] = p0[t];
+    for (int t = tid; t < d; t += kThreads) C[(int64_t)t * k] = p0[t];
     __syncthreads();
-    for (int64_t i = tid; i < n; i += kThreads) near[i] = sqdiff_row(P + i * d, C, d);
+    for (int64_t i = tid; i < n; i += kThreads) near[i] = sqdiff_col(P + i * d, C, k, 0, d);
     __syncthreads();
     for (int j = 1; j < k; ++j) {
       if (tid == 0) {
@@ -165,8 +182,19 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
       for (int64_t i = tid; i < n; i += kThreads) cdf[i] = __ddiv_rn(near[i], total);  // p = d2 / total
       __syncthreads();
       if (tid == 0) {
-        double acc = 0.0;  // cdf = p.cumsum() (sequential)
-        for (int64_t i = 0; i < n; ++i) {
+        double acc = 0.0;  // cdf = p.cumsum() (sequential; loads batched ahead of the adds)
+        int64_t i = 0;
+        for (; i + 8 <= n; i += 8) {
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = cdf[i + j];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc = __dadd_rn(acc, v[j]);
+            cdf[i + j] = acc;
+          }
+        }
+        for (; i < n; ++i) {
           acc = __dadd_rn(acc, cdf[i]);
           cdf[i] = acc;
         }
@@ -182,15 +210,14 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
       }
       __syncthreads();
       const double* pj = P + s_pick * d;
-      double* cj = C + (int64_t)j * d;
-      for (int t = tid; t < d; t += kThreads) cj[t] = pj[t];
+      for (int t = tid; t < d; t += kThreads) C[(int64_t)t * k + j] = pj[t];
       __syncthreads();
-      for (int64_t i = tid; i < n; i += kThreads) near[i] = fmin(near[i], sqdiff_row(P + i * d, cj, d));
+      for (int64_t i = tid; i < n; i += kThreads) near[i] = fmin(near[i], sqdiff_col(P + i * d, C, k, j, d));
       __syncthreads();
     }
   } else {
     const double* ci = init + (int64_t)r * k * d;
-    for (int64_t u = tid; u < (int64_t)k * d; u += kThreads) C[u] = ci[u];
+    for (int64_t u = tid; u < (int64_t)k * d; u += kThreads) C[(u % d) * k + u / d] = ci[u];
     __syncthreads();
   }
 
@@ -202,22 +229,23 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
     const int lane = tid & 31, warp = tid >> 5;
     for (int64_t it = 0; it < max_iters; ++it) {
       for (int j = tid; j < k; j += kThreads) {
-        cc[j] = sq_row(C + (int64_t)j * d, d);
+        cc[j] = sq_col(C, k, j, d);
         counts[j] = 0;
       }
       __syncthreads();
       // assignment: one warp per point, lanes over centroids, first argmin
+      double* p = pbuf + (size_t)warp * d;
       for (int64_t i = warp; i < n; i += kThreads / 32) {
-        const double* p = P + i * d;
+        for (int t = lane; t < d; t += 32) p[t] = P[i * d + t];
+        __syncwarp();
         double best = INFINITY;
         int bj = 0;
         for (int j0 = 0; j0 < k; j0 += 32) {
           const int j = j0 + lane;
           double dist = INFINITY;
           if (j < k) {
-            const double* c = C + (int64_t)j * d;
-            double dot = 0.0;
-            for (int t = 0; t < d; ++t) dot = fma(p[t], c[t], dot);
+            double dot = 0.0;  // C is d x k: the warp's 32 centroids are contiguous per coordinate
+            for (int t = 0; t < d; ++t) dot = fma(p[t], C[(int64_t)t * k + j], dot);
             dist = fmax(__dsub_rn(__dadd_rn(pp[i], cc[j]), 2.0 * dot), 0.0);
           }
           double v = dist;
@@ -241,6 +269,7 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
           near[i] = best;
           atomicAdd(&counts[bj], 1);
         }
+        __syncwarp();  // p is overwritten by the next point
       }
       __syncthreads();
       if (tid == 0) {
@@ -262,13 +291,13 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
       __syncthreads();
       // centroid_j = points[labels == j].mean(axis=0): sum in point order, then / count
       for (int64_t u = tid; u < (int64_t)k * d; u += kThreads) {
-        const int j = (int)(u / d), t = (int)(u % d);
+        const int t = (int)(u / k), j = (int)(u % k);
         const int cnt = counts[j];
         if (cnt > 0) {
           const int* mj = members + offs[j];
           double s = 0.0;
           for (int m = 0; m < cnt; ++m) s = __dadd_rn(s, P[(int64_t)mj[m] * d + t]);
-          C[u] = __ddiv_rn(s, (double)cnt);
+          C[(int64_t)t * k + j] = __ddiv_rn(s, (double)cnt);
         }
       }
       __syncthreads();
@@ -279,7 +308,7 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
           int64_t far = 0;  // first argmax of point_d2
           for (int64_t i = 1; i < n; ++i)
             if (near[i] > near[far]) far = i;
-          for (int t = 0; t < d; ++t) C[(int64_t)j * d + t] = P[far * d + t];
+          for (int t = 0; t < d; ++t) C[(int64_t)t * k + j] = P[far * d + t];
           near[far] = 0.0;
           rep = 1;
         }
@@ -296,7 +325,8 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
   }
   for (int64_t i = tid; i < n; i += kThreads) labels_out[(int64_t)r * n + i] = status == 0 ? lab[i] : 0;
   if (centroids_out)
-    for (int64_t u = tid; u < (int64_t)k * d; u += kThreads) centroids_out[(int64_t)r * k * d + u] = C[u];
+    for (int64_t u = tid; u < (int64_t)k * d; u += kThreads)
+      centroids_out[(int64_t)r * k * d + u] = C[(u % d) * k + u / d];
   if (tid == 0) {
     inertia_out[r] = inertia;
     iters_out[r] = iters;
@@ -326,9 +356,23 @@ void run_replicates(const double* points, int64_t n, int d, int k, int reps, con
   DeviceView dPcg(pcg, first ? sizeof(uint64_t) * 4 * reps : 0, device, s);
   DeviceView dInit(first ? nullptr : init, first ? 0 : sizeof(double) * reps * k * d, device, s);
   const size_t c_bytes = sizeof(double) * k * d;
-  const size_t head = (((size_t)k * 16 + 15) / 16) * 16;  // cc + counts + offs
-  const bool c_smem = head + c_bytes <= 200 * 1024;
-  const size_t smem = head + (c_smem ? c_bytes : 0);
+  const size_t limit = 200 * 1024;
+  SmemPlan sp;
+  sp.bytes = (((size_t)k * 16 + 15) / 16) * 16 + sizeof(double) * (kThreads / 32) * d;  // cc, counts, offs, points
+  if (sp.bytes > limit) fail(CSC_ERR_INVALID, "kmeans: k or d too large for the device kernel");
+  auto place = [&](int64_t& off, size_t bytes) {
+    bytes = (bytes + 15) / 16 * 16;
+    if (sp.bytes + bytes <= limit) {
+      off = (int64_t)sp.bytes;
+      sp.bytes += bytes;
+    }
+  };
+  place(sp.near, sizeof(double) * n);
+  place(sp.cdf, sizeof(double) * n);
+  place(sp.lab, sizeof(int) * n);
+  place(sp.C, c_bytes);
+  const bool c_smem = sp.C >= 0;
+  const size_t smem = sp.bytes;
   Scratch pp(sizeof(double) * n, s), Cg(c_smem ? 16 : c_bytes * reps, s), near(sizeof(double) * n * reps, s),
       cdf(sizeof(double) * n * reps, s), lab(sizeof(int) * n * reps, s), mem(sizeof(int) * n * reps, s),
       inert(sizeof(double) * reps, s), its(sizeof(int64_t) * reps, s), st(sizeof(int) * reps, s);
@@ -340,7 +384,7 @@ void run_replicates(const double* points, int64_t n, int d, int k, int reps, con
   k_kmeans_rep<<<reps, kThreads, smem, s>>>(
       dP.as<double>(), pp.as<double>(), n, d, k, first ? dFirst.as<int64_t>() : nullptr,
       first ? dPcg.as<uint64_t>() : nullptr, first ? nullptr : dInit.as<double>(), max_iters, tol, Cg.as<double>(),
-      near.as<double>(), cdf.as<double>(), lab.as<int>(), mem.as<int>(), c_smem ? 1 : 0, dLab.as<int64_t>(),
+      near.as<double>(), cdf.as<double>(), lab.as<int>(), mem.as<int>(), sp, dLab.as<int64_t>(),
       centroids_out ? dCen.as<double>() : nullptr, inert.as<double>(), its.as<int64_t>(), st.as<int>());
   CSC_LAUNCHED();
   dLab.finish();
