@@ -59,6 +59,14 @@ def filter_bytes(N: int, nnz: int, w: int, s: int, p: int) -> float:
     return (b_csr + 3.0 * N * w * s) + (p - 1) * (b_csr + 5.0 * N * w * s)
 
 
+def _ncu_dram_pct(config: str, dtype: str):
+    """ncu gpu__dram_throughput (% of ncu's peak) of the K2 launches, from profiles/ncu_traffic.json."""
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if not tf.exists():
+        return None
+    return json.loads(tf.read_text()).get(f"{config}_{dtype}_dram_throughput_pct")
+
+
 def peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -343,6 +351,8 @@ def run_ours(args, cfg):
         "algorithmic_unit": "SURVEY.md 8(d) B_step(d) = B_csr + 5 N d s per step launch (B_first on the first); "
                             "one launch per step when the block is one panel",
         "kernel_stream_bytes_per_launch": step_bytes / max(step_launches, 1),
+        "frac_of_8tbs": (achieved / 8000.0) if achieved else None,  # report against both peaks
+        "ncu_dram_throughput_pct": _ncu_dram_pct(args.config, cfg["dtype"]),
         "kernel_share_of_step": (step_ms / args.steps) / ms if ms > 0 else None,
         "recurrence": "clenshaw" if _lib.get_option("recurrence") == 0 else "forward",
         # K2 is bound by the neighbour-gather traffic through L2 (deg x row bytes per step), not by
@@ -369,7 +379,6 @@ def run_ours(args, cfg):
         "config": workload_config(cfg, N, nnz, d, world, {"panel_plan": _lib.get_option("panel_width") or "auto"}),
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpub,
         "clocks": clocks.summary(), "csc": csc,
-        "frac_of_8tbs": (achieved / 8000.0) if achieved else None,
     }
     print(json.dumps(line), flush=True)
 
