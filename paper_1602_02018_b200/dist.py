@@ -128,14 +128,23 @@ class DeviceBackend:
             return a.contiguous()
         return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
 
+    def normal_columns(self, rng, n: int, w: int, cols: slice):
+        """This rank's columns of the next n x w block of numpy's stream (every rank draws the
+        whole block, so the ranks see the reference's single stream), drawn on the GPU."""
+        from ._signals import device_normal_block, device_rng_available, normal_block
+
+        if not device_rng_available():
+            return np.ascontiguousarray(normal_block(rng, n, w)[:, cols])
+        return device_normal_block(rng, n, w, self.dev.index)[:, cols].contiguous()
+
     def count(self, filt: PolyFilter, R: np.ndarray) -> float:
         if R.shape[1] == 0:
             return 0.0
         c = coeff_array(filt)
-        Rd = np.ascontiguousarray(R, dtype=np.float64)
+        Rd = self._dev(R)
         out = C.c_double(0.0)
-        _lib.call("csc_eigencount", self.op.handle, _lib.ptr(c), int(c.size), _lib.ptr(Rd), int(Rd.shape[1]),
-                  int(Rd.shape[1]), _lib.CSC_F64, C.byref(out), self.stream())
+        _lib.call("csc_eigencount", self.op.handle, _lib.ptr(c), int(c.size), Rd.data_ptr(), int(Rd.shape[1]),
+                  int(Rd.shape[1]), _lib.dtype_code(Rd.dtype), C.byref(out), self.stream())
         return float(out.value)
 
     def filter_rowsq(self, filt: PolyFilter, R: np.ndarray):
@@ -235,6 +244,14 @@ def sharded_assign(backend, soft_local, col0: int, grp: Group):
     return labels.astype(np.int64), fallback
 
 
+def _normal_columns(backend, rng, n: int, w: int, cols: slice):
+    """This rank's columns of the next n x w normal block; every rank draws the whole block
+    (identical stream), on the device when the backend can."""
+    if hasattr(backend, "normal_columns"):
+        return backend.normal_columns(rng, n, w, cols)
+    return np.ascontiguousarray(normal_block(rng, n, w)[:, cols])
+
+
 def estimate_lambda_k_sharded(backend, N: int, k: int, order: int, ds: int | None, rng, grp: Group,
                               max_steps: int = 20, refine: bool = False):
     """Dichotomy of spectrum.py:90-140 with the probe columns sharded over ranks."""
@@ -245,8 +262,7 @@ def estimate_lambda_k_sharded(backend, N: int, k: int, order: int, ds: int | Non
 
     def probe(lam):
         filt = design_lowpass(min(lam, 2.0 - 1e-12), order, damping="jackson")
-        block = normal_block(rng, N, ds)  # every rank draws the full block: identical stream
-        cnt = sharded_count(backend, filt, np.ascontiguousarray(block[:, cols]), grp)
+        cnt = sharded_count(backend, filt, _normal_columns(backend, rng, N, ds, cols), grp)
         trace.append((float(lam), cnt))
         return cnt
 
@@ -270,7 +286,9 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
     N = num_nodes
     prm = params.resolve(N)
     t_run = time.perf_counter()
+    timings: dict[str, float] = {}
     warnings: list[str] = []
+    t0 = time.perf_counter()
     if prm.lambda_k is not None:
         lam, trace, warn, source = float(prm.lambda_k), [], False, "override"
     else:
@@ -280,17 +298,21 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
         source = "estimated"
         if warn:
             warnings.append("lambda_k bracket fallback")
+    timings["probe"] = time.perf_counter() - t0
     low = design_lowpass(lam, prm.p, damping=prm.damping)
     high = matched_highpass(low)
+    t0 = time.perf_counter()
     dcols = column_slice(prm.d, grp.world, grp.rank)
-    signals = normal_block(substream(prm.seed, "signals"), N, prm.d)
-    F, zero_rows = sharded_features(backend, low, np.ascontiguousarray(signals[:, dcols]), grp)
-    del signals
+    F, zero_rows = sharded_features(backend, low, _normal_columns(backend, substream(prm.seed, "signals"), N,
+                                                                  prm.d, dcols), grp)
     if zero_rows.size:
         warnings.append(f"{zero_rows.size} zero-norm feature rows")
+    timings["filter"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     sampling = draw_sampling(N, prm.n, substream(prm.seed, "sampling"), exclude=zero_rows)
     rows = np.concatenate(grp.all_gather(backend.gather(F, sampling.indices)), axis=1)
     labeling = backend.kmeans(rows, prm.kmeans)
+    timings["kmeans"] = time.perf_counter() - t0
     counts = np.bincount(labeling.labels, minlength=prm.k)
     if np.any(counts == 0):
         from .pipeline import DegenerateClusteringError
@@ -299,9 +321,11 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
     reduced = labels_to_indicators(labeling.labels, prm.k, prm.n)
     icfg = InterpolationConfig(highpass=high, gamma=prm.gamma, solver_tol=prm.solver_tol,
                                solver_max_iters=prm.solver_max_iters)
+    t0 = time.perf_counter()
     kcols = column_slice(prm.k, grp.world, grp.rank)
     X, info = backend.block_cg(icfg, sampling, np.ascontiguousarray(reduced[:, kcols]))
     labels, fallback = sharded_assign(backend, X, kcols.start, grp)
+    timings["interpolate"] = time.perf_counter() - t0
     its = np.concatenate(grp.all_gather_var(info.iterations))
     res = np.concatenate(grp.all_gather_var(info.residuals))
     conv = np.concatenate(grp.all_gather_var(info.converged.astype(np.uint8))).astype(bool)
@@ -315,7 +339,7 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
         "solver_residuals": res.tolist(), "solver_converged": conv.tolist(), "ridge": icfg.ridge,
         "zero_feature_rows": zero_rows.tolist(), "assign_fallback_nodes": fallback.tolist(), "warnings": warnings,
         "ranks": grp.world, "columns_per_rank": {"d": dcols.stop - dcols.start, "k": kcols.stop - kcols.start},
-        "timings": {"total": time.perf_counter() - t_run},
+        "timings": {**timings, "total": time.perf_counter() - t_run},
     }
     return ClusterResult(labels=labels, soft=X, diagnostics=diagnostics, num_clusters=prm.k)
 
