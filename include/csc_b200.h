@@ -188,7 +188,7 @@ int csc_kmeans_lloyd(const double* points, int64_t n, int d, const double* init,
                      int device, void* stream);
 
 /* `replicates` independent k-means runs, concurrently (one CTA each).  Seeding:
- *   first_index != NULL: k-means++ (kmeans.py:52-61) -- replicate r's first
+ *   first_index != NULL (host array, as pcg_states): k-means++ (kmeans.py:52-61) -- replicate r's first
  *     centroid is row first_index[r] (the host's rng.integers(q)) and its D^2
  *     draws come from the PCG64 state pcg_states[4r..4r+3] = {state_hi, state_lo,
  *     inc_hi, inc_lo} taken after that draw, with numpy's arithmetic (pairwise
@@ -234,7 +234,7 @@ int csc_set_exponential_tables(const uint64_t* ke, const double* we, const doubl
 /* Stochastic block model edges on the device, bit-identical to the reference's
  * generator (sbm.py:83-100, 118-155) from the PCG64 state of
  * default_rng(seed).  The npairs community pairs (a <= b, in the reference's
- * order, pairs that draw nothing left out) each give: cells (candidate node
+ * order, pairs that draw nothing left out; host arrays) each give: cells (candidate node
  * pairs, > 0), log1m_q = log1p(-q) for its edge probability q in (0, 1/3)
  * (computed by the caller with the C library, as numpy does), batch (the
  * reference's gap batch size), diag (1 for a == b), row_first (first node of
