@@ -214,7 +214,7 @@ def run_ours(args, cfg):
     from paper_1602_02018_b200 import _lib
     from paper_1602_02018_b200.dist import DeviceBackend, Group, sharded_features
     from paper_1602_02018_b200.features import RandomSignals, build_features
-    from paper_1602_02018_b200._signals import normal_block, pinned_empty
+    from paper_1602_02018_b200._signals import normal_block
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -286,7 +286,8 @@ def run_ours(args, cfg):
     filt = P.design_lowpass(lam, P_ORDER)
 
     # inputs: this rank's d signal columns (seeded per rank), resident in HBM for `value`
-    host = pinned_empty((N, d))
+    host_t = torch.empty((N, d), dtype=torch.float64, pin_memory=True)  # raises if pinning fails
+    host = host_t.numpy()
     normal_block(np.random.default_rng(1000 + rank), N, d, host)
     dtype_t = torch.float32 if cfg["dtype"] == "float32" else torch.float64
     X = torch.from_numpy(host).to(f"cuda:{local}").to(dtype_t)
@@ -326,7 +327,8 @@ def run_ours(args, cfg):
     value = world * work / (ms / 1e3) / 1e9
 
     # e2e through the public API with host buffers (pinned signals in, features out)
-    rows_out = pinned_empty((N, d))
+    rows_t = torch.empty((N, d), dtype=torch.float64, pin_memory=True)
+    rows_out = rows_t.numpy()
     signals = RandomSignals(matrix=host, distribution="gaussian", seed=None)
 
     def step_e2e():
@@ -341,14 +343,33 @@ def run_ours(args, cfg):
         step_e2e()
     barrier()
     torch.cuda.synchronize()
+    calls = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
+        t1 = time.perf_counter()
         step_e2e()
+        calls.append((time.perf_counter() - t1) * 1e3)  # step_e2e returns with the result on the host
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
+    # the host link this run saw (a slow or mis-placed box shows up here, not only in e2e)
+    dev_t = torch.empty((N, d), dtype=torch.float64, device=f"cuda:{local}")
+    link = {}
+    for name, fn in (("h2d_gbs", lambda: dev_t.copy_(host_t, non_blocking=True)),
+                     ("d2h_gbs", lambda: rows_t.copy_(dev_t, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        link[name] = 3 * host.nbytes / (time.perf_counter() - t0) / 1e9
+    del dev_t
     e2e = {"value": world * work / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(host.nbytes),
            "d2h_bytes_per_step": int(rows_out.nbytes + N), "ms_per_step": e2e_s * 1e3,
-           "api": "paper_1602_02018_b200.build_features(op, lowpass, signals) on pinned host fp64 arrays"}
+           "api": "paper_1602_02018_b200.build_features(op, lowpass, signals) on pinned host fp64 arrays",
+           "host_pinned": bool(host_t.is_pinned() and rows_t.is_pinned()),
+           "ms_per_call": [round(c, 2) for c in calls],
+           "link_gbs_measured": link}
 
     if rank != 0:
         return
