@@ -7,8 +7,9 @@ not shipped to the GPU box):
         python tests/golden/make_golden.py [--c2]
 
 Outputs (committed, small): tests/golden/graphs.npz, filter_c1.npz,
-pipeline_c1.npz and, with --c2, pipeline_c2.npz (scalars, indices and labels
-only; the reference takes ~2.5 min there).
+pipeline_c1.npz, formats.npz (the reference's own on-disk formats: feature dump,
+labels CSV, result JSON, dichotomy trace CSV) and, with --c2, pipeline_c2.npz
+(scalars, indices and labels only; the reference takes ~2.5 min there).
 """
 
 from __future__ import annotations
@@ -103,12 +104,42 @@ def pipeline(N, k, d, seed, full: bool):
     return out
 
 
+def formats():
+    """Bytes written by the reference's save_features (features.py:101-116), save_labels_csv /
+    save_json (result.py:50-58) and trace_to_csv (spectrum.py:143-152)."""
+    import tempfile
+
+    from cscluster import features as rfeat, spectrum as rspec
+
+    rng = np.random.default_rng(21)
+    rows = rng.standard_normal((7, 3))
+    rows[2] = 0.0
+    prov = {"distribution": "gaussian", "filter": {"cutoff": 0.5, "order": 50}, "seed": 5}
+    fm = rfeat.FeatureMatrix(rows=rows, normalized=True, zero_rows=np.array([2], dtype=np.int64), provenance=prov)
+    g, _ = ref.sbm_generate(sbm_config(1000, 20))
+    op = ref.laplacian_op(g)
+    res = ref.run_csc(op, ref.CscParams(k=20, d=int(math.ceil(4 * math.log(1000))), seed=0))
+    est = rspec.estimate_lambda_k(op, 20, rng=substream(0, "probe"))
+    with tempfile.TemporaryDirectory() as td:
+        td = Path(td)
+        rfeat.save_features(fm, td / "f.bin")
+        res.save_labels_csv(td / "labels.csv")
+        res.save_json(td / "result.json")
+        rspec.trace_to_csv(est, td / "trace.csv")
+        blob = {name: np.frombuffer((td / name).read_bytes(), dtype=np.uint8)
+                for name in ("f.bin", "labels.csv", "result.json", "trace.csv")}
+    np.savez_compressed(OUT / "formats.npz", features_dump=blob["f.bin"], labels_csv=blob["labels.csv"],
+                        result_json=blob["result.json"], trace_csv=blob["trace.csv"], rows=rows,
+                        provenance=np.frombuffer(json.dumps(prov).encode(), dtype=np.uint8))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
     args = ap.parse_args()
     graphs()
     filter_c1()
+    formats()
     np.savez_compressed(OUT / "pipeline_c1.npz", **pipeline(1000, 20, int(math.ceil(4 * math.log(1000))), 0, True))
     if args.c2:
         np.savez_compressed(OUT / "pipeline_c2.npz", **pipeline(100_000, 20, int(math.ceil(4 * math.log(1e5))), 0, False))

@@ -7,7 +7,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import D_C1, GOLDEN, golden, sbm_config
+from conftest import D_C1, GOLDEN, ROOT, golden, sbm_config
 from gpu_util import c1_op, options
 import paper_1602_02018_b200 as P
 from paper_1602_02018_b200.kmeans import Labeling
@@ -108,3 +108,30 @@ def test_lambda_fallback_flag_matches_oracle():
     lam, trace, warn = O.estimate_lambda_k(oracle_csr(g), 2, 50, None, O.substream(3, "probe"), max_steps=6)
     assert r.diagnostics["lambda_warning"] is warn
     assert r.diagnostics["lambda_k_hat"] == lam
+
+
+def test_result_and_trace_files_match_reference(tmp_path):
+    """save_labels_csv / save_json (result.py:50-58) and trace_to_csv (spectrum.py:143-152)
+    against the files the reference wrote for the same C1 run."""
+    import csv
+    import io
+    import json
+
+    from paper_1602_02018_b200._rng import substream
+
+    gold = np.load(ROOT / "tests" / "golden" / "formats.npz")
+    r = P.run_csc(c1_op(), P.CscParams(k=20, d=D_C1, seed=0))
+    r.save_labels_csv(tmp_path / "labels.csv")
+    assert (tmp_path / "labels.csv").read_bytes() == bytes(gold["labels_csv"])
+    r.save_json(tmp_path / "result.json")
+    got, ref = json.loads((tmp_path / "result.json").read_text()), json.loads(bytes(gold["result_json"]).decode())
+    assert sorted(got) == sorted(ref) and got["labels"] == ref["labels"]
+    assert sorted(got["diagnostics"]) == sorted(ref["diagnostics"])
+    est = P.estimate_lambda_k(c1_op(), 20, rng=substream(0, "probe"))
+    P.spectrum.trace_to_csv(est, tmp_path / "trace.csv")
+    rows_got = list(csv.reader(io.StringIO((tmp_path / "trace.csv").read_text())))
+    rows_ref = list(csv.reader(io.StringIO(bytes(gold["trace_csv"]).decode())))
+    assert rows_got[0] == rows_ref[0] == ["lambda", "count"] and len(rows_got) == len(rows_ref)
+    for (lg, cg), (lr, cr) in zip(rows_got[1:], rows_ref[1:]):
+        assert lg == lr  # identical probe frequencies (repr)
+        assert abs(float(cg) - float(cr)) <= 1e-9 * abs(float(cr))

@@ -247,3 +247,27 @@ def test_new_abi_argument_validation():
     with pytest.raises(ValueError, match="1/3"):
         _lib.call("csc_sbm_edges", 1, 2, 3, 5, 1, *[_lib.ptr(x) for x in args], 0, None, None, _lib.ptr(n_e), None,
                   0, None)
+
+
+def test_feature_dump_format_matches_reference():
+    """save_features writes the reference's bytes (features.py:101-116); load_features reads its dump."""
+    import json
+    from pathlib import Path
+
+    from conftest import ROOT
+    from paper_1602_02018_b200.features import FeatureMatrix, load_features, save_features
+
+    gold = np.load(Path(ROOT) / "tests" / "golden" / "formats.npz")
+    prov = json.loads(bytes(gold["provenance"]).decode())
+    fm = FeatureMatrix(rows=gold["rows"], normalized=True, zero_rows=np.array([2], dtype=np.int64), provenance=prov)
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "f.bin"
+        save_features(fm, p)
+        assert p.read_bytes() == bytes(gold["features_dump"])
+        q = Path(td) / "ref.bin"
+        q.write_bytes(bytes(gold["features_dump"]))
+        back = load_features(q)
+    assert np.array_equal(back.rows, gold["rows"]) and back.zero_rows.tolist() == [2]
+    assert back.normalized is True and back.provenance == prov
