@@ -248,18 +248,24 @@ def run_ours(args, cfg):
 
     sharded = world > 1 or args.force_sharded
     csc = None
+    res = None
     lam = 0.5
     if sharded and not args.no_csc:
         from paper_1602_02018_b200.dist import DeviceBackend, run_csc_sharded
 
         walls = []
-        for _ in range(2):  # first call pays one-off module loading / pool growth; report both
-            barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            res = run_csc_sharded(DeviceBackend(op), N, P.CscParams(k=k, d=d, seed=0), grp)
-            torch.cuda.synchronize()
-            walls.append(max_over_ranks(time.perf_counter() - t0))
+        try:
+            for _ in range(2):  # first call pays one-off module loading / pool growth; report both
+                barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = run_csc_sharded(DeviceBackend(op), N, P.CscParams(k=k, d=d, seed=0), grp)
+                torch.cuda.synchronize()
+                walls.append(max_over_ranks(time.perf_counter() - t0))
+        except Exception as exc:  # the CSC timing is secondary: never lose the metric line over it
+            res = None
+            csc = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    if sharded and not args.no_csc and res is not None:
         lam = res.diagnostics["lambda_k_hat"]
         csc = {"wall_s": walls[1], "wall_s_first_call": walls[0], "stages_s": res.diagnostics["timings"],
                "lambda_k_hat": lam, "probe_iterations": res.diagnostics["probe_iterations"],
@@ -335,9 +341,9 @@ def run_ours(args, cfg):
         if not sharded:
             build_features(op, filt, signals, out=rows_out)
         else:
-            Xh = torch.from_numpy(host).to(f"cuda:{local}").to(dtype_t)
+            Xh = host_t.to(f"cuda:{local}", non_blocking=True).to(dtype_t)  # pinned H2D, cast on the GPU
             Fl, _ = sharded_features(backend, filt, Xh, grp)
-            torch.from_numpy(rows_out).copy_(Fl)
+            rows_t.copy_(Fl.to(torch.float64))  # cast on the GPU, pinned D2H
 
     for _ in range(max(1, args.warmup)):
         step_e2e()
