@@ -372,7 +372,10 @@ def run_ours(args, cfg):
     del dev_t
     e2e = {"value": world * work / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(host.nbytes),
            "d2h_bytes_per_step": int(rows_out.nbytes + N), "ms_per_step": e2e_s * 1e3,
-           "api": "paper_1602_02018_b200.build_features(op, lowpass, signals) on pinned host fp64 arrays",
+           "api": ("paper_1602_02018_b200.build_features(op, lowpass, signals) on pinned host fp64 arrays"
+                   if not sharded else
+                   "paper_1602_02018_b200.dist.sharded_features (this rank's columns, NCCL row-norm exchange) "
+                   "on pinned host fp64 arrays"),
            "host_pinned": bool(host_t.is_pinned() and rows_t.is_pinned()),
            "ms_per_call": [round(c, 2) for c in calls],
            "link_gbs_measured": link}
