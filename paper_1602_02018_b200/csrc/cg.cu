@@ -15,6 +15,8 @@
 // partials, beta + freeze bookkeeping, and P = R + beta P.
 #include <algorithm>
 #include <cmath>
+#include <memory>
+#include <vector>
 
 #include "filter.cuh"
 
@@ -171,6 +173,31 @@ __global__ void k_cg_finish(ColState st, int wc, int64_t iters, double* __restri
   its[c] = st.active[c] ? iters : st.conv_at[c];
 }
 
+// residuals / flags / iterations of the current columns, written at their panel columns cmap[c]
+__global__ void k_cg_finish_map(ColState st, int wc, int64_t iters, const int* __restrict__ cmap,
+                                double* __restrict__ resid, uint8_t* __restrict__ conv, int64_t* __restrict__ its) {
+  const int c = threadIdx.x;
+  if (c >= wc) return;
+  const int o = cmap[c];
+  const double r = sqrt(st.rs[c]);
+  resid[o] = r;
+  conv[o] = r <= sqrt(st.t2[c]) + kTiny ? 1 : 0;
+  its[o] = st.active[c] ? iters : st.conv_at[c];
+}
+
+// per-column state of the kept columns: dst[j] = src[map[j]]
+__global__ void k_gather_state(ColState src, ColState dst, const int* __restrict__ map, int wc) {
+  const int j = threadIdx.x;
+  if (j >= wc) return;
+  const int c = map[j];
+  dst.rs[j] = src.rs[c];
+  dst.t2[j] = src.t2[c];
+  dst.alpha[j] = src.alpha[c];
+  dst.beta[j] = src.beta[c];
+  dst.conv_at[j] = src.conv_at[c];
+  dst.active[j] = src.active[c];
+}
+
 template <typename T>
 __global__ void k_scatter_rhs(const double* __restrict__ reduced, int k, const int64_t* __restrict__ idx, int64_t n,
                               int c0, int wc, int pw, T* __restrict__ B) {
@@ -195,6 +222,49 @@ __global__ void k_mask(const int64_t* __restrict__ idx, int64_t n, int64_t N, ui
   }
 }
 
+// --- column compaction: once at most half of a panel's columns are still active, they
+// move into a panel half as wide (or narrower), so later filter passes stop paying for
+// frozen columns.  Per-column arithmetic is unchanged.
+
+// dst[:, j] = src[:, map[j]] for j < wc (zero padding up to pw_dst)
+template <typename T>
+__global__ void k_gather_cols(const T* __restrict__ src, int pw_src, T* __restrict__ dst, int pw_dst,
+                              const int* __restrict__ map, int wc, int64_t n) {
+  const int64_t total = n * pw_dst;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / pw_dst;
+    const int j = (int)(t - r * pw_dst);
+    dst[t] = j < wc ? src[r * pw_src + map[j]] : T(0);
+  }
+}
+
+// dst[:, map[j]] = src[:, j] for j < wc
+template <typename T>
+__global__ void k_scatter_cols(const T* __restrict__ src, int pw_src, T* __restrict__ dst, int pw_dst,
+                               const int* __restrict__ map, int wc, int64_t n) {
+  const int64_t total = n * wc;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / wc;
+    const int j = (int)(t - r * wc);
+    dst[r * pw_dst + map[j]] = src[r * pw_src + j];
+  }
+}
+
+// per-column state carved out of one allocation of `w` columns
+ColState carve_state(Scratch& mem, int w, cudaStream_t s) {
+  const size_t head = ((sizeof(double) * 4 * w + sizeof(int64_t) * w + w + 15) / 16) * 16;
+  mem.alloc(head + 16, s);
+  ColState st;
+  st.rs = mem.as<double>();
+  st.t2 = st.rs + w;
+  st.alpha = st.t2 + w;
+  st.beta = st.alpha + w;
+  st.conv_at = reinterpret_cast<int64_t*>(st.beta + w);
+  st.active = reinterpret_cast<uint8_t*>(st.conv_at + w);
+  st.nactive = reinterpret_cast<int*>(mem.as<char>() + head);
+  return st;
+}
+
 template <typename T>
 void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double ridge, const uint8_t* mask,
               const int64_t* idx, int64_t n, const double* reduced, int k, double tol, int64_t max_iters, int c0,
@@ -206,15 +276,8 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
   const int cg = colred_grid(g->device);
   const int cap = std::max(step_grid_cap(g->device), cg);
   Scratch part(sizeof(double) * (size_t)cap * pw, s);
-  Scratch colmem(sizeof(double) * 4 * pw + sizeof(int64_t) * pw + pw + 64, s);
-  ColState st;
-  st.rs = colmem.as<double>();
-  st.t2 = st.rs + pw;
-  st.alpha = st.t2 + pw;
-  st.beta = st.alpha + pw;
-  st.conv_at = reinterpret_cast<int64_t*>(st.beta + pw);
-  st.active = reinterpret_cast<uint8_t*>(st.conv_at + pw);
-  st.nactive = reinterpret_cast<int*>(colmem.as<char>() + ((sizeof(double) * 4 * pw + sizeof(int64_t) * pw + pw + 15) / 16) * 16);
+  auto colmem = std::make_unique<Scratch>();
+  ColState st = carve_state(*colmem, pw, s);
 
   // X = 0; R = P = B = M^T C  (sampling.py:142-149)
   CSC_CUDA(cudaMemsetAsync(Xp, 0, pb, s));
@@ -235,9 +298,23 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
   k_cg_init<<<wc, 256, 0, s>>>(part.as<double>(), cg, pw, wc, tol, st);
   CSC_LAUNCHED();
 
-  // per-thread pinned flag (cudaMallocHost/cudaFreeHost per call would synchronise the device)
+  // the current (possibly compacted) panel: its width, columns, buffers and the map
+  // from its columns to the caller's panel columns
+  int pw_cur = pw, wc_cur = wc;
+  T *Xc = Xp, *Rc = R.as<T>(), *Pc = P.as<T>(), *Psc = Ps.as<T>();
+  std::unique_ptr<Scratch> own[4];  // compacted X, R, P, Ps
+  std::vector<int> hmap(wc);
+  for (int c = 0; c < wc; ++c) hmap[c] = c;
+  Scratch cmap(sizeof(int) * pw, s), amap(sizeof(int) * pw, s);
+  CSC_CUDA(cudaMemcpyAsync(cmap.get(), hmap.data(), sizeof(int) * wc, cudaMemcpyHostToDevice, s));
+  const bool compact = g_opt.cg_compact.load() != 0;
+  const int min_pw = 32 / (int)sizeof(T);  // narrower rows cost as much per step (one 32-B sector)
+
+  // per-thread pinned staging (cudaMallocHost/cudaFreeHost per call would synchronise the device)
   static thread_local int* h_active = nullptr;
+  static thread_local uint8_t* h_flags = nullptr;
   if (!h_active) CSC_CUDA(cudaMallocHost(&h_active, sizeof(int)));
+  if (!h_flags) CSC_CUDA(cudaMallocHost(&h_flags, 256));
   int64_t iters = 0;
   CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
   CSC_CUDA(cudaStreamSynchronize(s));
@@ -248,22 +325,77 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
     ex.gamma = gamma;
     ex.ridge = ridge;
     ex.ap = AP.get();
-    const int fgrid = filter_panel<T>(g, hp, nc, P.as<T>(), Ps.as<T>(), nullptr, B0.as<T>(), B1.as<T>(),
-                                      Yacc.as<T>(), pw, wc, EPI_CGAP, ex, s);
-    k_cg_alpha<<<wc, 256, 0, s>>>(part.as<double>(), fgrid, pw, wc, st);
+    const int fgrid = filter_panel<T>(g, hp, nc, Pc, Psc, nullptr, B0.as<T>(), B1.as<T>(), Yacc.as<T>(), pw_cur,
+                                      wc_cur, EPI_CGAP, ex, s);
+    k_cg_alpha<<<wc_cur, 256, 0, s>>>(part.as<double>(), fgrid, pw_cur, wc_cur, st);
     CSC_LAUNCHED();
-    k_cg_update<T><<<cg, 256, 0, s>>>(Xp, R.as<T>(), P.as<T>(), AP.as<T>(), st.alpha, N, pw, wc, part.as<double>());
+    k_cg_update<T><<<cg, 256, 0, s>>>(Xc, Rc, Pc, AP.as<T>(), st.alpha, N, pw_cur, wc_cur, part.as<double>());
     CSC_LAUNCHED();
     ++iters;
-    k_cg_beta<<<wc, 256, 0, s>>>(part.as<double>(), cg, pw, wc, iters, st);
+    k_cg_beta<<<wc_cur, 256, 0, s>>>(part.as<double>(), cg, pw_cur, wc_cur, iters, st);
     CSC_LAUNCHED();
-    k_cg_direction<T><<<dgrid, 256, 0, s>>>(P.as<T>(), Ps.as<T>(), R.as<T>(), st.beta, g->dis, N, pw, wc);
+    k_cg_direction<T><<<dgrid, 256, 0, s>>>(Pc, Psc, Rc, st.beta, g->dis, N, pw_cur, wc_cur);
     CSC_LAUNCHED();
     CSC_CUDA(cudaMemcpyAsync(h_active, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
     CSC_CUDA(cudaStreamSynchronize(s));
+    const int nact = *h_active;
+    int want = min_pw;
+    while (want < nact) want *= 2;
+    if (!compact || nact == 0 || iters >= max_iters || want >= pw_cur) continue;
+    // ---- compaction: keep the active columns in a panel `want` wide
+    CSC_CUDA(cudaMemcpyAsync(h_flags, st.active, (size_t)wc_cur, cudaMemcpyDeviceToHost, s));
+    CSC_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> act, nmap;
+    for (int c = 0; c < wc_cur; ++c)
+      if (h_flags[c]) {
+        act.push_back(c);
+        nmap.push_back(hmap[c]);
+      }
+    if ((int)act.size() != nact) fail(CSC_ERR_CUDA, "block CG: active-column bookkeeping mismatch");
+    // final values of every current column (the kept ones are rewritten at the end)
+    k_cg_finish_map<<<1, 128, 0, s>>>(st, wc_cur, iters, cmap.as<int>(), resid, conv, its);
+    CSC_LAUNCHED();
+    const size_t nb = sizeof(T) * (size_t)N * want;
+    std::unique_ptr<Scratch> nxt[4];
+    for (auto& b : nxt) b = std::make_unique<Scratch>(nb, s);
+    CSC_CUDA(cudaMemcpyAsync(amap.get(), act.data(), sizeof(int) * nact, cudaMemcpyHostToDevice, s));
+    const int ggrid = (int)std::max<int64_t>(1, std::min<int64_t>((N * want + 255) / 256,
+                                                                   (int64_t)device_props(g->device).sms * 16));
+    T* cur[4] = {Xc, Rc, Pc, Psc};
+    for (int b = 0; b < 4; ++b) {
+      k_gather_cols<T><<<ggrid, 256, 0, s>>>(cur[b], pw_cur, nxt[b]->as<T>(), want, amap.as<int>(), nact, N);
+      CSC_LAUNCHED();
+    }
+    auto colmem_n = std::make_unique<Scratch>();
+    ColState stn = carve_state(*colmem_n, want, s);
+    k_gather_state<<<1, 128, 0, s>>>(st, stn, amap.as<int>(), nact);
+    CSC_LAUNCHED();
+    if (Xc != Xp) {  // columns leaving the compacted X go back to the caller's panel
+      k_scatter_cols<T><<<ggrid, 256, 0, s>>>(Xc, pw_cur, Xp, pw, cmap.as<int>(), wc_cur, N);
+      CSC_LAUNCHED();
+    }
+    for (int b = 0; b < 4; ++b) own[b] = std::move(nxt[b]);
+    Xc = own[0]->as<T>();
+    Rc = own[1]->as<T>();
+    Pc = own[2]->as<T>();
+    Psc = own[3]->as<T>();
+    colmem = std::move(colmem_n);
+    st = stn;
+    CSC_CUDA(cudaMemcpyAsync(st.nactive, h_active, sizeof(int), cudaMemcpyHostToDevice, s));
+    hmap = nmap;
+    CSC_CUDA(cudaMemcpyAsync(cmap.get(), hmap.data(), sizeof(int) * nact, cudaMemcpyHostToDevice, s));
+    CSC_CUDA(cudaStreamSynchronize(s));  // host vectors feeding async copies go out of scope
+    pw_cur = want;
+    wc_cur = nact;
   }
-  k_cg_finish<<<1, 128, 0, s>>>(st, wc, iters, resid, conv, its);
+  k_cg_finish_map<<<1, 128, 0, s>>>(st, wc_cur, iters, cmap.as<int>(), resid, conv, its);
   CSC_LAUNCHED();
+  if (Xc != Xp) {
+    const int ggrid = (int)std::max<int64_t>(1, std::min<int64_t>((N * wc_cur + 255) / 256,
+                                                                   (int64_t)device_props(g->device).sms * 16));
+    k_scatter_cols<T><<<ggrid, 256, 0, s>>>(Xc, pw_cur, Xp, pw, cmap.as<int>(), wc_cur, N);
+    CSC_LAUNCHED();
+  }
   *iters_run = std::max(*iters_run, iters);
 }
 

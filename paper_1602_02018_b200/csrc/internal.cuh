@@ -74,6 +74,7 @@ struct Options {
   std::atomic<int64_t> row_order{0};      // 0 interleaved row groups, 1 contiguous ranges per warp
   std::atomic<int64_t> l2_persist_pct{0}; // >0: keep the gathered panel in a persisting L2 window
   std::atomic<int64_t> persistent{1};     // 1: step grid = resident CTAs (grid-stride); 0: one CTA per row block
+  std::atomic<int64_t> cg_compact{1};     // block CG: move still-active columns into narrower panels
 };
 extern Options g_opt;
 

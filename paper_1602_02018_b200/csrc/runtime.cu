@@ -170,6 +170,7 @@ static std::atomic<int64_t>* option_slot(const char* key) {
   if (k == "unroll") return &g_opt.unroll;
   if (k == "l2_persist_pct") return &g_opt.l2_persist_pct;
   if (k == "persistent") return &g_opt.persistent;
+  if (k == "cg_compact") return &g_opt.cg_compact;
   if (k == "row_order") return &g_opt.row_order;
   return nullptr;
 }

@@ -244,3 +244,20 @@ def test_kmeans_random_seeding_matches_host_replicates():
         if best is None or inert < best[1]:
             best = (lab, inert, it)
     assert np.array_equal(a.labels, best[0]) and a.inertia == best[1] and a.iterations_run == best[2]
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-12), ("float32", 1e-5)])
+def test_block_cg_column_compaction_is_exact(c1_golden, dtype, tol):
+    """Moving still-active columns into narrower panels (cg_compact) keeps every column's CG:
+    same iteration counts and convergence flags, X equal up to reduction-order rounding."""
+    hp = P.matched_highpass(P.design_lowpass(float(c1_golden["lambda_k_hat"]), 50))
+    cfg = P.InterpolationConfig(highpass=hp)
+    samp = P.SamplingSet(indices=c1_golden["indices"], num_nodes=1000)
+    red = reduced_c1(c1_golden)
+    with options(cg_compact=0):
+        Xa, ia = P.interpolate_all(c1_op(dtype), cfg, samp, red)
+    with options(cg_compact=1):
+        Xb, ib = P.interpolate_all(c1_op(dtype), cfg, samp, red)
+    assert np.array_equal(ia.iterations, ib.iterations) and np.array_equal(ia.converged, ib.converged)
+    assert relerr(Xb, Xa) <= tol
+    assert len(set(ia.iterations.tolist())) > 1  # staggered convergence: compaction actually happened
