@@ -14,7 +14,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--dtype", default=None)
+ap.add_argument("--option", action="append", default=[], help="libcsc option key=value")
 args = ap.parse_args()
+from paper_1602_02018_b200 import _lib  # noqa: E402
+
+for kv in args.option:
+    key, val = kv.split("=")
+    _lib.set_option(key, int(val))
 cfg = CONFIGS[args.config]
 g, truth = make_graph(P, cfg)
 op = P.laplacian_op(g, dtype=args.dtype or cfg["dtype"])
