@@ -1,0 +1,61 @@
+"""Randomised parity (hypothesis): device graph build and filters against the oracle on messy
+edge lists -- duplicates in both directions, self loops (dropped), zero weights, isolated nodes."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings, strategies as st
+
+from conftest import relerr
+from oracle import cpu_ref as O
+import paper_1602_02018_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+WEIGHTS = st.one_of(st.sampled_from([0.0, 0.5, 1.0, 2.25, 3.0]),
+                    st.floats(min_value=1e-3, max_value=10.0, allow_nan=False, allow_infinity=False))
+
+
+@st.composite
+def edge_lists(draw):
+    n = draw(st.integers(min_value=2, max_value=60))
+    m = draw(st.integers(min_value=1, max_value=4 * n))
+    src = draw(st.lists(st.integers(0, n - 1), min_size=m, max_size=m))
+    dst = draw(st.lists(st.integers(0, n - 1), min_size=m, max_size=m))
+    w = draw(st.lists(WEIGHTS, min_size=m, max_size=m))
+    return n, np.array(src), np.array(dst), np.array(w, dtype=np.float64)
+
+
+def _oracle_csr(n, src, dst, w):
+    keep = src != dst  # self_loops="drop"
+    return O.build_csr(src[keep], dst[keep], w[keep], n)
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(edge_lists())
+def test_graph_build_matches_oracle(case):
+    n, src, dst, w = case
+    ref = _oracle_csr(n, src, dst, w)
+    g = P.build_graph(np.column_stack([src, dst, w]), num_nodes=n, self_loops="drop")
+    assert np.array_equal(g.indptr, ref.indptr) and np.array_equal(g.indices, ref.indices)
+    assert np.array_equal(g.weights, ref.weights) and np.array_equal(g.degrees, ref.degrees)
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(edge_lists(), st.sampled_from([1, 2, 5, 30]), st.integers(1, 9), st.integers(0, 1))
+def test_filter_matches_oracle(case, order, width, rec):
+    n, src, dst, w = case
+    ref = _oracle_csr(n, src, dst, w)
+    g = P.build_graph(np.column_stack([src, dst, w]), num_nodes=n, self_loops="drop")
+    X = np.random.default_rng(order * 31 + width).standard_normal((n, width))
+    filt = P.design_lowpass(0.7, order)
+    want = O.apply_filter(filt.coeffs, ref, X)
+    P._lib.set_option("recurrence", rec)
+    try:
+        got64 = P.apply_filter(filt, P.laplacian_op(g), X)
+        got32 = P.apply_filter(filt, P.laplacian_op(g, dtype="float32"), X)
+    finally:
+        P._lib.set_option("recurrence", 0)
+    assert relerr(got64, want) <= 1e-12
+    assert relerr(got32, want) <= 1e-4
