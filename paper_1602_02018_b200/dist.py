@@ -310,7 +310,10 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
     timings["filter"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     sampling = draw_sampling(N, prm.n, substream(prm.seed, "sampling"), exclude=zero_rows)
-    rows = np.concatenate(grp.all_gather(backend.gather(F, sampling.indices)), axis=1)
+    # ranks own different numbers of feature columns when d % world != 0: exchange the
+    # sampled rows column-major so the variable extent is the leading axis
+    part = np.ascontiguousarray(np.asarray(backend.gather(F, sampling.indices)).T)
+    rows = np.ascontiguousarray(np.concatenate(grp.all_gather_var(part), axis=0).T)
     labeling = backend.kmeans(rows, prm.kmeans)
     timings["kmeans"] = time.perf_counter() - t0
     counts = np.bincount(labeling.labels, minlength=prm.k)

@@ -147,8 +147,10 @@ def _run_sharded(grp):
     return res.labels, res.diagnostics["lambda_k_hat"], res.diagnostics["solver_iterations"], res.num_clusters
 
 
-def test_run_csc_sharded_matches_reference(c1_golden):
-    parts = run_world(_run_sharded)
+@pytest.mark.parametrize("world", [2, 3])
+def test_run_csc_sharded_matches_reference(c1_golden, world):
+    # world 3: uneven column slices (d = 28, k = 20, ds = 14 do not divide by 3)
+    parts = run_world(_run_sharded, world=world)
     for labels, lam, its, k in parts:
         assert lam == float(c1_golden["lambda_k_hat"])
         assert its == c1_golden["solver_iterations"].tolist()

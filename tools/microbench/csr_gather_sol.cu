@@ -1,0 +1,153 @@
+// Speed of light of K2's gathers on the real graph: read every CSR entry's neighbour row
+// (the `valid` leading floats of a `stride`-float panel row) in CSR order, exactly the
+// gather stream of one Chebyshev step, with nothing else (no S/X/O streams, no epilogue).
+//
+//   csr_gather_sol <indptr.bin> <indices.bin> [repeats]
+//
+// indptr/indices: raw int32 files (tools/dump_csr.py writes them for a BASELINE config).
+// Each configuration: LPR lanes (16 B each) per edge, 32/LPR edges per warp, U edges in
+// flight per lane group, B CTAs of 256 threads per SM (grid-stride).  Prints the time per
+// pass, row gathers/s and gathered bytes/s (valid bytes).  Also times a sequential copy of
+// the panel (HBM reference) for the same bytes.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o csr_gather_sol csr_gather_sol.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                          \
+  do {                                                                 \
+    cudaError_t e = (x);                                               \
+    if (e != cudaSuccess) {                                            \
+      printf("%s: %s\n", #x, cudaGetErrorString(e));                   \
+      exit(1);                                                         \
+    }                                                                  \
+  } while (0)
+
+template <int LPR, int U>
+__global__ void __launch_bounds__(256) k_gather(const float* __restrict__ G, int stride, int valid,
+                                                const int* __restrict__ idx, long nnz, float* __restrict__ sink) {
+  constexpr int EPW = 32 / LPR;  // edges per warp per slot
+  const int lane = threadIdx.x & 31, sub = lane % LPR, grp = lane / LPR;
+  const bool on = grp < EPW && sub * 4 < valid;
+  const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long e0 = warp * EPW * U; e0 < nnz; e0 += nw * EPW * U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long e = e0 + u * EPW + grp;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (on && e < nnz) v[u] = __ldg(reinterpret_cast<const float4*>(G + (size_t)__ldg(idx + e) * stride) + sub);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc.x += v[u].x;
+      acc.y += v[u].y;
+      acc.z += v[u].z;
+      acc.w += v[u].w;
+    }
+  }
+  if (acc.x + acc.y + acc.z + acc.w == 12345.f) sink[0] = acc.x;  // keep the loads alive
+}
+
+__global__ void k_copy(const float4* __restrict__ a, float4* __restrict__ b, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+static std::vector<int> load(const char* path) {
+  FILE* f = fopen(path, "rb");
+  if (!f) {
+    printf("cannot open %s\n", path);
+    exit(1);
+  }
+  fseek(f, 0, SEEK_END);
+  long bytes = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  std::vector<int> v(bytes / 4);
+  if (fread(v.data(), 4, v.size(), f) != v.size()) exit(1);
+  fclose(f);
+  return v;
+}
+
+template <int LPR, int U>
+static void run(const float* G, int stride, int valid, const int* idx, long nnz, long n, float* sink, int blocks_per_sm,
+                int sms, int reps, const char* tag) {
+  const int grid = sms * blocks_per_sm;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_gather<LPR, U><<<grid, 256>>>(G, stride, valid, idx, nnz, sink);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) k_gather<LPR, U><<<grid, 256>>>(G, stride, valid, idx, nnz, sink);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  const double us = 1e3 * ms / reps;
+  const int vb = ((valid + 3) / 4) * 16;
+  printf("%-8s stride %3d floats valid %3d  LPR %2d U %d  %2d CTAs/SM  %8.1f us/pass  %6.2f G rows/s  %6.2f TB/s valid  "
+         "(panel %.0f MB)\n",
+         tag, stride, valid, LPR, U, blocks_per_sm, us, nnz / us / 1e3, nnz * (double)vb / us / 1e6,
+         n * (double)stride * 4 / 1e6);
+  CK(cudaEventDestroy(e0));
+  CK(cudaEventDestroy(e1));
+}
+
+int main(int argc, char** argv) {
+  if (argc < 3) {
+    printf("usage: %s indptr.bin indices.bin [repeats]\n", argv[0]);
+    return 1;
+  }
+  std::vector<int> ip = load(argv[1]), ix = load(argv[2]);
+  const int reps = argc > 3 ? atoi(argv[3]) : 10;
+  const long n = (long)ip.size() - 1, nnz = (long)ix.size();
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  printf("N=%ld nnz=%ld (mean degree %.2f), %d SMs\n", n, nnz, (double)nnz / n, sms);
+  float *G, *sink, *B;
+  int* idx;
+  const size_t panel = (size_t)n * 128 * sizeof(float);
+  CK(cudaMalloc(&G, panel));
+  CK(cudaMalloc(&B, panel));
+  CK(cudaMemset(G, 0, panel));
+  CK(cudaMalloc(&sink, 64));
+  CK(cudaMalloc(&idx, sizeof(int) * nnz));
+  CK(cudaMemcpy(idx, ix.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+
+  // sequential HBM reference: copy of the N x 64 fp32 panel
+  {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const long n4 = n * 64 / 4;
+    k_copy<<<sms * 8, 256>>>(reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(B), n4);
+    CK(cudaEventRecord(e0));
+    for (int r = 0; r < reps; ++r)
+      k_copy<<<sms * 8, 256>>>(reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(B), n4);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    printf("copy     N x 64 fp32 panel: %.1f us, %.2f TB/s (read + write)\n", 1e3 * ms / reps,
+           2.0 * n4 * 16 / (1e-3 * ms / reps) / 1e12);
+  }
+  // K2's layouts: d=56 (one 64-wide panel), d=36 (64-wide), d=28 (32-wide), 16-wide, 128-wide
+  for (int bps : {6, 8}) {
+    run<16, 4>(G, 64, 56, idx, nnz, n, sink, bps, sms, reps, "d=56");
+    run<16, 8>(G, 64, 56, idx, nnz, n, sink, bps, sms, reps, "d=56");
+    run<16, 4>(G, 64, 36, idx, nnz, n, sink, bps, sms, reps, "d=36");
+    run<16, 4>(G, 64, 64, idx, nnz, n, sink, bps, sms, reps, "d=64");
+    run<8, 4>(G, 32, 28, idx, nnz, n, sink, bps, sms, reps, "d=28");
+    run<8, 8>(G, 32, 28, idx, nnz, n, sink, bps, sms, reps, "d=28");
+    run<4, 4>(G, 16, 16, idx, nnz, n, sink, bps, sms, reps, "d=16");
+    run<32, 4>(G, 128, 100, idx, nnz, n, sink, bps, sms, reps, "d=100");
+  }
+  // compact 56-float stride (no padding): LPR 14 lanes active of 16
+  run<16, 4>(G, 56, 56, idx, nnz, n, sink, 6, sms, reps, "d=56c");
+  run<16, 8>(G, 56, 56, idx, nnz, n, sink, 8, sms, reps, "d=56c");
+  return 0;
+}
