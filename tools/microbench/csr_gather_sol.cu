@@ -12,6 +12,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o csr_gather_sol csr_gather_sol.cu
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -53,6 +54,96 @@ __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ G, int
   if (acc.x + acc.y + acc.z + acc.w == 12345.f) sink[0] = acc.x;  // keep the loads alive
 }
 
+// cp.async ring: per warp D batches of B slots (slot = 32 lanes x 16 B = EPW edges' row slices).
+// Gathers land in shared memory, so the in-flight depth is not bounded by registers; the
+// neighbour indices of a batch are loaded one iteration before its copies are issued.
+template <int LPR, int D>
+__global__ void __launch_bounds__(256) k_gather_cpa(const float* __restrict__ G, int stride, int valid,
+                                                    const int* __restrict__ idx, long nnz, float* __restrict__ sink) {
+  constexpr int EPW = 32 / LPR, B = 4;
+  extern __shared__ float4 ring[];  // [warps][D][B][32]
+  const int lane = threadIdx.x & 31, sub = lane % LPR, grp = lane / LPR, wib = threadIdx.x >> 5;
+  const bool on = grp < EPW && sub * 4 < valid;
+  float4* my = ring + (size_t)wib * D * B * 32;
+  const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  // batch t of this warp covers edges ((warp + t * nw) * B + b) * EPW + grp, b < B
+  auto edge = [&](long t, int b) { return ((warp + t * nw) * B + b) * EPW + grp; };
+  int nxt[B];
+  auto load_idx = [&](long t) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const long e = edge(t, b);
+      nxt[b] = (on && e < nnz) ? __ldg(idx + e) : -1;
+    }
+  };
+  auto issue = [&](int slot) {
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (nxt[b] >= 0) {
+        const float4* src = reinterpret_cast<const float4*>(G + (size_t)nxt[b] * stride) + sub;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(my + (slot * B + b) * 32 + lane)),
+                     "l"(src)
+                     : "memory");
+      }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const long nb = (nnz / (EPW * B) + nw) / nw + 1;
+  for (int t = 0; t < D - 1; ++t) {
+    load_idx(t);
+    issue(t);
+  }
+  load_idx(D - 1);
+  for (long t = 0; t < nb; ++t) {
+    issue((int)((t + D - 1) % D));
+    load_idx(t + D);
+    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const long e = edge(t, b);
+      if (on && e < nnz) {
+        const float4 v = my[((t % D) * B + b) * 32 + lane];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (acc.x + acc.y + acc.z + acc.w == 12345.f) sink[0] = acc.x;
+}
+
+template <int LPR, int D>
+static void run_cpa(const float* G, int stride, int valid, const int* idx, long nnz, long n, float* sink,
+                    int blocks_per_sm, int sms, int reps, const char* tag) {
+  const int grid = sms * blocks_per_sm;
+  const size_t smem = (size_t)8 * D * 4 * 32 * 16;
+  CK(cudaFuncSetAttribute(k_gather_cpa<LPR, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather_cpa<LPR, D>, 256, smem));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_gather_cpa<LPR, D><<<grid, 256, smem>>>(G, stride, valid, idx, nnz, sink);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) k_gather_cpa<LPR, D><<<grid, 256, smem>>>(G, stride, valid, idx, nnz, sink);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  const double us = 1e3 * ms / reps;
+  const int vb = ((valid + 3) / 4) * 16;
+  printf("%-8s cp.async ring D=%2d  stride %3d valid %3d  LPR %2d  %d CTAs/SM (resident %d, %zu KB smem/CTA)  %8.1f us/pass  "
+         "%6.2f G rows/s  %6.2f TB/s valid\n",
+         tag, D, stride, valid, LPR, blocks_per_sm, occ, smem / 1024, us, nnz / us / 1e3, nnz * (double)vb / us / 1e6);
+  CK(cudaEventDestroy(e0));
+  CK(cudaEventDestroy(e1));
+}
+
 __global__ void k_copy(const float4* __restrict__ a, float4* __restrict__ b, long n) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) b[i] = a[i];
 }
@@ -79,6 +170,9 @@ static void run(const float* G, int stride, int valid, const int* idx, long nnz,
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<LPR, U>, 256, 0));
+  if (occ < blocks_per_sm) printf("  (only %d CTAs/SM resident)\n", occ);
   k_gather<LPR, U><<<grid, 256>>>(G, stride, valid, idx, nnz, sink);
   CK(cudaDeviceSynchronize());
   CK(cudaEventRecord(e0));
@@ -113,7 +207,15 @@ int main(int argc, char** argv) {
   const size_t panel = (size_t)n * 128 * sizeof(float);
   CK(cudaMalloc(&G, panel));
   CK(cudaMalloc(&B, panel));
-  CK(cudaMemset(G, 0, panel));
+  {
+    std::vector<float> h((size_t)n * 128);
+    uint32_t x = 12345u;
+    for (auto& v : h) {
+      x = x * 1664525u + 1013904223u;
+      v = (float)(x >> 8) * (1.0f / 16777216.0f) - 0.5f;
+    }
+    CK(cudaMemcpy(G, h.data(), panel, cudaMemcpyHostToDevice));
+  }
   CK(cudaMalloc(&sink, 64));
   CK(cudaMalloc(&idx, sizeof(int) * nnz));
   CK(cudaMemcpy(idx, ix.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
@@ -135,6 +237,18 @@ int main(int argc, char** argv) {
     printf("copy     N x 64 fp32 panel: %.1f us, %.2f TB/s (read + write)\n", 1e3 * ms / reps,
            2.0 * n4 * 16 / (1e-3 * ms / reps) / 1e12);
   }
+  const bool quick = getenv("SOL_QUICK") != nullptr;
+  run<16, 4>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
+  run<16, 4>(G, 64, 56, idx, nnz, n, sink, 8, sms, reps, "d=56");
+  run<16, 6>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
+  run_cpa<16, 2>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
+  run_cpa<16, 2>(G, 64, 56, idx, nnz, n, sink, 4, sms, reps, "d=56");
+  run_cpa<16, 3>(G, 64, 56, idx, nnz, n, sink, 4, sms, reps, "d=56");
+  run_cpa<16, 4>(G, 64, 56, idx, nnz, n, sink, 3, sms, reps, "d=56");
+  run_cpa<16, 6>(G, 64, 56, idx, nnz, n, sink, 2, sms, reps, "d=56");
+  run_cpa<8, 2>(G, 32, 28, idx, nnz, n, sink, 6, sms, reps, "d=28");
+  run_cpa<8, 3>(G, 32, 28, idx, nnz, n, sink, 4, sms, reps, "d=28");
+  if (quick) return 0;
   // K2's layouts: d=56 (one 64-wide panel), d=36 (64-wide), d=28 (32-wide), 16-wide, 128-wide
   for (int bps : {6, 8}) {
     run<16, 4>(G, 64, 56, idx, nnz, n, sink, bps, sms, reps, "d=56");
