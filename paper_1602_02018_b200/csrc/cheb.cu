@@ -105,8 +105,11 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
   const int gbase = lane & ~(LPR - 1);
   const int col0 = sub * VEC;
   const bool lane_on = col0 < a.wc;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // 32-bit row / group / vector-offset arithmetic (n * LPR < 2^32 for every supported
+  // size): fewer registers in the neighbour loop
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  const V* __restrict__ Gv = static_cast<const V*>(a.G) + sub;
 
   const T* __restrict__ G = static_cast<const T*>(a.G);
   const T* S = static_cast<const T*>(a.S);
@@ -131,10 +134,11 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
   // row-group schedule: interleaved (warp w takes groups w, w + nwarps, ...) or
   // contiguous (each warp owns one contiguous run of groups, so an SM works on
   // neighbouring rows and their shared neighbours can hit in L1)
-  const int64_t ngroups = (a.n + GPW - 1) / GPW;
-  int64_t gfirst, gstep, glast;
+  const int n = (int)a.n;
+  const int ngroups = (n + GPW - 1) / GPW;
+  int gfirst, gstep, glast;
   if (a.contig) {
-    const int64_t per = (ngroups + nwarps - 1) / nwarps;
+    const int per = (ngroups + nwarps - 1) / nwarps;
     gfirst = warp * per;
     glast = min(ngroups, gfirst + per);
     gstep = 1;
@@ -143,20 +147,19 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
     glast = ngroups;
     gstep = nwarps;
   }
-  int64_t gi = gfirst;
+  int gi = gfirst;
   int32_t nbeg = 0, nend = 0;  // indptr pair of the next row group (prefetched)
-  if (G != nullptr && gi < glast && gi * GPW + grp < a.n) {
+  if (G != nullptr && gi < glast && gi * GPW + grp < n) {
     nbeg = __ldg(a.indptr + gi * GPW + grp);
     nend = __ldg(a.indptr + gi * GPW + grp + 1);
   }
   for (; gi < glast; gi += gstep) {
-    const int64_t rb = gi * GPW;
-    const int64_t row = rb + grp;
-    const bool rok = row < a.n;
+    const int row = gi * GPW + grp;
+    const bool rok = row < n;
     const bool on = rok && lane_on;
-    const int32_t beg = nbeg;
     const int cnt = nend - nbeg;
-    const size_t off = (size_t)row * PW + col0;
+    const uint32_t voff = (uint32_t)row * LPR + sub;  // this lane's vector in row-local streams
+    const size_t off = (size_t)voff * VEC;
 
     // 1. row-local operands: loaded after the neighbour loop (latency hidden by
     //    the other resident warps; keeping them live across it costs occupancy)
@@ -170,13 +173,15 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
     for (int c = 0; c < VEC; ++c) acc[c] = T(0);
     if (G != nullptr) {
       const int maxcnt = __reduce_max_sync(FULL, cnt);
+      const int32_t* ip = indices + nbeg;
+      const T* wp = wv + nbeg;
       int32_t jj[UC];
       T ww[UC];
 #pragma unroll
       for (int u = 0; u < UC; ++u) {
         const int e = u * LPR + sub;
-        jj[u] = e < cnt ? ld_csr(HINTS, indices + beg + e) : -1;
-        if constexpr (!UNIT) ww[u] = e < cnt ? ld_csr(HINTS, wv + beg + e) : T(0);
+        jj[u] = e < cnt ? ld_csr(HINTS, ip + e) : -1;
+        if constexpr (!UNIT) ww[u] = e < cnt ? ld_csr(HINTS, wp + e) : T(0);
       }
       for (int base = 0; base < maxcnt; base += CH) {
         int32_t jn[UC];
@@ -185,8 +190,8 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 #pragma unroll
         for (int u = 0; u < UC; ++u) {
           const int e = base + CH + u * LPR + sub;
-          jn[u] = (more && e < cnt) ? ld_csr(HINTS, indices + beg + e) : -1;
-          if constexpr (!UNIT) wn[u] = (more && e < cnt) ? ld_csr(HINTS, wv + beg + e) : T(0);
+          jn[u] = (more && e < cnt) ? ld_csr(HINTS, ip + e) : -1;
+          if constexpr (!UNIT) wn[u] = (more && e < cnt) ? ld_csr(HINTS, wp + e) : T(0);
         }
         int32_t jc[CH];
         T wc[CH];
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
           gv[k] = VT::zero();
-          if (jc[k] >= 0 && lane_on) gv[k] = __ldg(reinterpret_cast<const V*>(G + (size_t)jc[k] * PW + col0));
+          if (jc[k] >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)jc[k] * LPR);
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -224,8 +229,8 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 
     // 3. prefetch the next row group's indptr pair
     {
-      const int64_t nrow = (gi + gstep) * GPW + grp;
-      if (G != nullptr && gi + gstep < glast && nrow < a.n) {
+      const int nrow = (gi + gstep) * GPW + grp;
+      if (G != nullptr && gi + gstep < glast && nrow < n) {
         nbeg = __ldg(a.indptr + nrow);
         nend = __ldg(a.indptr + nrow + 1);
       } else {
