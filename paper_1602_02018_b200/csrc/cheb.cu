@@ -197,9 +197,10 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
         T wc[CH];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {  // slot k is entry k / LPR of lane gbase + k % LPR
-          jc[k] = LPR == 1 ? jj[k] : __shfl_sync(FULL, jj[k / LPR], gbase + k % LPR);
+          // width-LPR shuffles: the source lane k % LPR is relative to this row's lane segment
+          jc[k] = LPR == 1 ? jj[k] : __shfl_sync(FULL, jj[k / LPR], k % LPR, LPR);
           wc[k] = T(1);
-          if constexpr (!UNIT) wc[k] = LPR == 1 ? ww[k] : __shfl_sync(FULL, ww[k / LPR], gbase + k % LPR);
+          if constexpr (!UNIT) wc[k] = LPR == 1 ? ww[k] : __shfl_sync(FULL, ww[k / LPR], k % LPR, LPR);
         }
         V gv[CH];
 #pragma unroll
@@ -455,6 +456,8 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   a.contig = g_opt.row_order.load() == 1;
   constexpr int VEC = 16 / sizeof(T);
   const int lpr = pw / VEC;
+  if (a.n > 0 && (uint64_t)a.n * (uint64_t)lpr >= (1ull << 32))
+    fail(CSC_ERR_INVALID, "panel too large for 32-bit vector offsets (rows x lanes >= 2^32)");
   const int threads = (int)g_opt.block_threads.load();
   const bool prof = g_opt.profile.load() != 0 && a.G != nullptr;
   cudaEvent_t e0 = nullptr;

@@ -54,6 +54,66 @@ __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ G, int
   if (acc.x + acc.y + acc.z + acc.w == 12345.f) sink[0] = acc.x;  // keep the loads alive
 }
 
+// 32-byte lanes: ld.global.nc.v8.f32 (LDG.E.ENL2.256), LPR lanes of 32 B per row
+template <int LPR, int U>
+__global__ void __launch_bounds__(256) k_gather8(const float* __restrict__ G, int stride, int valid,
+                                                 const int* __restrict__ idx, long nnz, float* __restrict__ sink) {
+  constexpr int EPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, sub = lane % LPR, grp = lane / LPR;
+  const bool on = grp < EPW && sub * 8 < valid;
+  const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (long e0 = warp * EPW * U; e0 < nnz; e0 += nw * EPW * U) {
+    float v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long e = e0 + u * EPW + grp;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[u][c] = 0.f;
+      if (on && e < nnz) {
+        const float* p = G + (size_t)__ldg(idx + e) * stride + sub * 8;
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(v[u][0]), "=f"(v[u][1]), "=f"(v[u][2]), "=f"(v[u][3]), "=f"(v[u][4]), "=f"(v[u][5]),
+                       "=f"(v[u][6]), "=f"(v[u][7])
+                     : "l"(p));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] += v[u][c];
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) t += acc[c];
+  if (t == 12345.f) sink[0] = t;
+}
+
+template <int LPR, int U>
+static void run8(const float* G, int stride, int valid, const int* idx, long nnz, long n, float* sink, int blocks_per_sm,
+                 int sms, int reps, const char* tag) {
+  const int grid = sms * blocks_per_sm;
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather8<LPR, U>, 256, 0));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_gather8<LPR, U><<<grid, 256>>>(G, stride, valid, idx, nnz, sink);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) k_gather8<LPR, U><<<grid, 256>>>(G, stride, valid, idx, nnz, sink);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  const double us = 1e3 * ms / reps;
+  printf("%-8s v8 (32-B lanes) stride %3d valid %3d  LPR %2d U %d  %d CTAs/SM (resident %d)  %8.1f us/pass  %6.2f G rows/s\n",
+         tag, stride, valid, LPR, U, blocks_per_sm, occ, us, nnz / us / 1e3);
+  CK(cudaEventDestroy(e0));
+  CK(cudaEventDestroy(e1));
+}
+
 // cp.async ring: per warp D batches of B slots (slot = 32 lanes x 16 B = EPW edges' row slices).
 // Gathers land in shared memory, so the in-flight depth is not bounded by registers; the
 // neighbour indices of a batch are loaded one iteration before its copies are issued.
@@ -248,6 +308,14 @@ int main(int argc, char** argv) {
   run_cpa<16, 6>(G, 64, 56, idx, nnz, n, sink, 2, sms, reps, "d=56");
   run_cpa<8, 2>(G, 32, 28, idx, nnz, n, sink, 6, sms, reps, "d=28");
   run_cpa<8, 3>(G, 32, 28, idx, nnz, n, sink, 4, sms, reps, "d=28");
+  run8<8, 1>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
+  run8<8, 2>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
+  run8<8, 2>(G, 64, 56, idx, nnz, n, sink, 8, sms, reps, "d=56");
+  run8<8, 3>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
+  run8<8, 4>(G, 64, 56, idx, nnz, n, sink, 4, sms, reps, "d=56");
+  run8<4, 2>(G, 32, 28, idx, nnz, n, sink, 6, sms, reps, "d=28");
+  run8<4, 2>(G, 32, 28, idx, nnz, n, sink, 8, sms, reps, "d=28");
+  run<8, 4>(G, 32, 28, idx, nnz, n, sink, 6, sms, reps, "d=28");
   if (quick) return 0;
   // K2's layouts: d=56 (one 64-wide panel), d=36 (64-wide), d=28 (32-wide), 16-wide, 128-wide
   for (int bps : {6, 8}) {
