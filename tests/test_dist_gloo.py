@@ -93,7 +93,7 @@ def _worker(rank, world, port, fn, out):
 
 
 def run_world(fn, world=2):
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), fn, out), nprocs=world, join=True)
     return [out[r] for r in range(world)]
