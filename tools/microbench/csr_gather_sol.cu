@@ -298,6 +298,36 @@ int main(int argc, char** argv) {
            2.0 * n4 * 16 / (1e-3 * ms / reps) / 1e12);
   }
   const bool quick = getenv("SOL_QUICK") != nullptr;
+  if (getenv("SOL_SPLIT")) {
+    // source-split passes: the edges into each of P source ranges, in CSR order, one pass per
+    // range (a range's gather rows can stay in L2 while its pass runs)
+    for (int P : {1, 2, 3, 4}) {
+      std::vector<std::vector<int>> parts(P);
+      for (long e = 0; e < nnz; ++e) parts[(long)ix[e] * P / n].push_back(ix[e]);
+      double tot = 0.0;
+      for (int q = 0; q < P; ++q) {
+        int* d = nullptr;
+        CK(cudaMalloc(&d, sizeof(int) * parts[q].size()));
+        CK(cudaMemcpy(d, parts[q].data(), sizeof(int) * parts[q].size(), cudaMemcpyHostToDevice));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        k_gather<16, 4><<<sms * 6, 256>>>(G, 64, 56, d, (long)parts[q].size(), sink);
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(e0));
+        for (int r = 0; r < reps; ++r) k_gather<16, 4><<<sms * 6, 256>>>(G, 64, 56, d, (long)parts[q].size(), sink);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        tot += 1e3 * ms / reps;
+        CK(cudaFree(d));
+      }
+      printf("split P=%d: d=56 (64-float stride) gathers in %d source ranges of %.0f MB: %.1f us total\n", P, P,
+             n * 256.0 / P / 1e6, tot);
+    }
+    return 0;
+  }
   run<16, 4>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
   run<16, 4>(G, 64, 56, idx, nnz, n, sink, 8, sms, reps, "d=56");
   run<16, 6>(G, 64, 56, idx, nnz, n, sink, 6, sms, reps, "d=56");
