@@ -59,3 +59,33 @@ def test_filter_matches_oracle(case, order, width, rec):
         P._lib.set_option("recurrence", 0)
     assert relerr(got64, want) <= 1e-12
     assert relerr(got32, want) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype,pw,tol", [("float64", 64, 1e-12), ("float32", 128, 1e-4), ("float64", 8, 1e-12)])
+@pytest.mark.parametrize("rec", [0, 1])
+def test_wide_panels_heavy_weighted_rows(dtype, pw, rec, tol):
+    """32-lane panel rows (512 B: 8-slot neighbour chunks, only lanes < 8 hold indices) on a
+    weighted graph with heavy-tailed degrees (up to ~70), so rows span many 8-slot chunks and the
+    warp-uniform chunk loop ends mid-chunk; every width up to two panels."""
+    rng = np.random.default_rng(11)
+    n = 700
+    deg = np.minimum(rng.pareto(1.5, n) * 6 + 1, 60).astype(int)
+    deg[rng.choice(n, 25, replace=False)] = 0  # rows with incoming edges only
+    src = np.repeat(np.arange(n), deg)
+    dst = rng.integers(0, n, src.size)
+    w = rng.choice([0.5, 1.0, 2.25, 3.0], src.size)
+    ref = _oracle_csr(n, src, dst, w)
+    assert np.diff(ref.indptr).max() > 48
+    g = P.build_graph(np.column_stack([src, dst, w]), num_nodes=n, self_loops="drop")
+    op = P.laplacian_op(g, dtype=dtype)
+    filt = P.design_lowpass(0.6, 20)
+    old_pw, old_rec = P._lib.get_option("panel_width"), P._lib.get_option("recurrence")
+    P._lib.set_option("panel_width", pw)
+    P._lib.set_option("recurrence", rec)
+    try:
+        for width in (1, pw // 2 + 3, pw, pw + 5):
+            X = rng.standard_normal((n, width))
+            assert relerr(P.apply_filter(filt, op, X), O.apply_filter(filt.coeffs, ref, X)) <= tol, width
+    finally:
+        P._lib.set_option("panel_width", old_pw)
+        P._lib.set_option("recurrence", old_rec)
