@@ -111,6 +111,33 @@ int csc_graph_info(const csc_graph* g, int64_t* num_nodes, int64_t* nnz, int* dt
 int csc_graph_export(const csc_graph* g, int32_t* indptr, int32_t* indices, double* weights,
                      double* degrees, double* d_inv_sqrt, void* stream);
 
+/* ---- edge-list text I/O (host, multi-threaded) ---------------------------- */
+/* Replaces read_edge_list's line loop (graph.py:177-214).  Parses "src dst [weight]" lines,
+ * '#' comments and the "# nodes N" header with the reference's classification (universal
+ * newlines, ASCII str.strip/split).  Tokens are converted natively only where the value is
+ * provably Python's int()/float(); every other line is reported as "complex" (line number,
+ * byte range, reserved row slot or -1 for a comment) for the caller to parse with the
+ * reference's own rules, so values, row order and errors are the reference's.
+ * nthreads <= 0: all hardware threads. */
+typedef struct csc_edges csc_edges;
+int csc_edgelist_read(const char* path, int nthreads, csc_edges** out);
+/* header_nodes: value of the last natively parsed "# nodes N" line (-1: none); header_line:
+ * its line number (0: none). */
+int csc_edgelist_info(const csc_edges* e, int64_t* num_rows, int64_t* num_complex, int64_t* header_nodes,
+                      int64_t* header_line);
+/* Rows in file order (src, dst as exact doubles, weight); complex_row[r] = 1 marks a slot
+ * reserved for a complex line. */
+int csc_edgelist_rows(const csc_edges* e, double* src, double* dst, double* weights, uint8_t* complex_row);
+int csc_edgelist_complex(const csc_edges* e, int64_t* line_numbers, int64_t* row_slots, int64_t* byte_offsets,
+                         int64_t* byte_lengths);
+int csc_edgelist_destroy(csc_edges* e);
+/* Replaces write_edge_list (graph.py:215-225): "# nodes N" then "i j repr(w)" per stored
+ * entry with i < j in CSR order; repr() is Python's shortest round-trip float format. */
+int csc_edgelist_write(const char* path, int64_t num_nodes, const int32_t* indptr, const int32_t* indices,
+                       const double* weights, int nthreads);
+/* Python repr() of a double as csc_edgelist_write prints it (test hook; cap >= 32). */
+int csc_float_repr(double v, char* out, int cap, int* len);
+
 /* ---- operator / filter (K2) --------------------------------------------- */
 /* Y = L X for an N x ncols block.  Replaces LaplacianOp.apply (graph.py:147-155). */
 int csc_laplacian_apply(const csc_graph* g, const void* X, int64_t ldx, void* Y, int64_t ldy,

@@ -72,6 +72,55 @@ def csr_digest(g: Csr) -> str:
     return h.hexdigest()
 
 
+class EdgeListError(ValueError):
+    """The reference's GraphError for edge-list lines (graph.py:203, 209)."""
+
+
+def parse_edge_text(text: str, name: str = "<path>"):
+    """read_edge_list's line loop (graph.py:188-212) over already-decoded text: (rows E x 3
+    float64, header node count or None).  ``text.splitlines(keepends=True)`` restricted to
+    '\n', '\r\n' and '\r' is Python's universal-newline iteration of the file object."""
+    import io
+
+    rows = []
+    header_nodes = None
+    for lineno, line in enumerate(io.StringIO(text, newline=None), start=1):
+        stripped = line.strip()
+        if not stripped:
+            continue
+        if stripped.startswith("#"):
+            parts = stripped[1:].split()
+            if len(parts) == 2 and parts[0] == "nodes":
+                try:
+                    header_nodes = int(parts[1])
+                except ValueError:
+                    pass
+            continue
+        parts = stripped.split()
+        if len(parts) not in (2, 3):
+            raise EdgeListError(f"{name}:{lineno}: expected 'src dst [weight]', got {stripped!r}")
+        try:
+            i = int(parts[0])
+            j = int(parts[1])
+            w = float(parts[2]) if len(parts) == 3 else 1.0
+        except ValueError as exc:
+            raise EdgeListError(f"{name}:{lineno}: {exc}") from None
+        rows.append((i, j, w))
+    return np.array(rows, dtype=np.float64).reshape(len(rows), 3), header_nodes
+
+
+def format_edge_list(num_nodes: int, indptr, indices, weights) -> bytes:
+    """write_edge_list's bytes (graph.py:215-225): W.tocoo() of a canonical CSR is its storage
+    order, so entries with row < col in CSR order, one "i j repr(w)" line each."""
+    out = [f"# nodes {num_nodes}\n"]
+    for i in range(num_nodes):
+        for k in range(int(indptr[i]), int(indptr[i + 1])):
+            j = int(indices[k])
+            if i < j:
+                out.append(f"{i} {j} {float(weights[k])!r}\n")
+    return "".join(out).encode("utf-8")
+
+
 def laplacian_apply(g: Csr, x: np.ndarray, W=None, dis=None) -> np.ndarray:
     """x - dis * (W @ (dis * x))  (graph.py:147-155)."""
     x = np.asarray(x, dtype=np.float64)

@@ -42,6 +42,13 @@ SIGNATURES: dict[str, list] = {
     "csc_graph_destroy": [_p],
     "csc_graph_info": [_p, _p, _p, _p, _p],
     "csc_graph_export": [_p, _p, _p, _p, _p, _p, _p],
+    "csc_edgelist_read": [C.c_char_p, _i32, _p],
+    "csc_edgelist_info": [_p, _p, _p, _p, _p],
+    "csc_edgelist_rows": [_p, _p, _p, _p, _p],
+    "csc_edgelist_complex": [_p, _p, _p, _p, _p],
+    "csc_edgelist_destroy": [_p],
+    "csc_edgelist_write": [C.c_char_p, _i64, _p, _p, _p, _i32],
+    "csc_float_repr": [_f64, _p, _i32, _p],
     "csc_laplacian_apply": [_p, _p, _i64, _p, _i64, _i32, _i32, _p],
     "csc_cheb_filter": [_p, _p, _i32, _p, _i64, _p, _i64, _i32, _i32, _p],
     "csc_eigencount": [_p, _p, _i32, _p, _i64, _i32, _i32, _p, _p],

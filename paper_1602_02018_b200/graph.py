@@ -268,39 +268,74 @@ def apply_laplacian(op: LaplacianOp, x):
     return op.apply(x)
 
 
+def parse_edge_list(path: str | Path) -> tuple[np.ndarray, int | None]:
+    """The parse of read_edge_list (graph.py:188-212): rows (E x 3 float64, file order) and
+    the ``# nodes N`` header value (None when absent).
+
+    The line loop runs in the library (``csc_edgelist_read``, multi-threaded); lines whose
+    tokens it does not convert itself (non-ASCII, underscores, inf/nan, wrong token counts,
+    ...) come back as "complex" and are parsed here with the reference's own rules, in file
+    order, so values, row order and the first error raised match the reference."""
+    path = Path(path)
+    h = C.c_void_p()
+    _lib.call("csc_edgelist_read", str(path).encode(), 0, C.byref(h))
+    try:
+        nr, ncx, hn, hl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.call("csc_edgelist_info", h, C.byref(nr), C.byref(ncx), C.byref(hn), C.byref(hl))
+        src, dst, w = np.empty(nr.value), np.empty(nr.value), np.empty(nr.value)
+        cx = np.empty(nr.value, dtype=np.uint8)
+        _lib.call("csc_edgelist_rows", h, _lib.ptr(src), _lib.ptr(dst), _lib.ptr(w), _lib.ptr(cx))
+        lines, slots, offs, lens = (np.empty(ncx.value, dtype=np.int64) for _ in range(4))
+        _lib.call("csc_edgelist_complex", h, _lib.ptr(lines), _lib.ptr(slots), _lib.ptr(offs), _lib.ptr(lens))
+    finally:
+        _lib.call("csc_edgelist_destroy", h)
+    header_nodes = int(hn.value) if hl.value > 0 else None
+    header_line = int(hl.value)
+    keep = np.ones(nr.value, dtype=bool)
+    if ncx.value:
+        with path.open("rb") as fh:
+            for lineno, slot, off, ln in zip(lines.tolist(), slots.tolist(), offs.tolist(), lens.tolist()):
+                fh.seek(off)
+                stripped = fh.read(ln).decode("utf-8").strip()
+                if not stripped or stripped.startswith("#"):
+                    if slot >= 0:
+                        keep[slot] = False
+                    parts = stripped[1:].split() if stripped else []
+                    if len(parts) == 2 and parts[0] == "nodes":
+                        try:
+                            value = int(parts[1])
+                        except ValueError:
+                            pass
+                        else:
+                            if lineno > header_line:
+                                header_nodes, header_line = value, lineno
+                    continue
+                parts = stripped.split()
+                if len(parts) not in (2, 3):
+                    raise GraphError(f"{path}:{lineno}: expected 'src dst [weight]', got {stripped!r}")
+                try:
+                    i, j = int(parts[0]), int(parts[1])
+                    wt = float(parts[2]) if len(parts) == 3 else 1.0
+                except ValueError as exc:
+                    raise GraphError(f"{path}:{lineno}: {exc}") from None
+                src[slot], dst[slot], w[slot] = float(i), float(j), wt
+    rows = np.column_stack([src[keep], dst[keep], w[keep]])
+    return rows, header_nodes
+
+
 def read_edge_list(path: str | Path, num_nodes: int | None = None) -> Graph:
     """Parse ``src dst [weight]`` lines (``#`` comments, ``# nodes N`` header), as graph.py:177-214."""
-    path = Path(path)
-    rows: list[tuple[int, int, float]] = []
-    header_nodes = None
-    with path.open("r", encoding="utf-8") as fh:
-        for lineno, line in enumerate(fh, start=1):
-            text = line.strip()
-            if not text:
-                continue
-            if text.startswith("#"):
-                parts = text[1:].split()
-                if len(parts) == 2 and parts[0] == "nodes" and parts[1].lstrip("-").isdigit():
-                    header_nodes = int(parts[1])
-                continue
-            parts = text.split()
-            if len(parts) not in (2, 3):
-                raise GraphError(f"{path}:{lineno}: expected 'src dst [weight]', got {text!r}")
-            try:
-                rows.append((int(parts[0]), int(parts[1]), float(parts[2]) if len(parts) == 3 else 1.0))
-            except ValueError as exc:
-                raise GraphError(f"{path}:{lineno}: {exc}") from None
+    rows, header_nodes = parse_edge_list(path)
     if num_nodes is None:
         num_nodes = header_nodes
-    return build_graph(np.array(rows, dtype=np.float64).reshape(len(rows), 3), num_nodes=num_nodes)
+    return build_graph(rows, num_nodes=num_nodes, self_loops="error")
 
 
 def write_edge_list(graph: Graph, path: str | Path) -> None:
-    """One ``src dst weight`` line per undirected edge (i < j), with a ``# nodes N`` header."""
-    counts = np.diff(graph.indptr)
-    rows = np.repeat(np.arange(graph.num_nodes), counts)
-    keep = rows < graph.indices
-    with Path(path).open("w", encoding="utf-8") as fh:
-        fh.write(f"# nodes {graph.num_nodes}\n")
-        for i, j, w in zip(rows[keep], graph.indices[keep], graph.weights[keep]):
-            fh.write(f"{int(i)} {int(j)} {float(w)!r}\n")
+    """One ``src dst weight`` line per undirected edge (i < j) in CSR order, after a ``# nodes N``
+    header (graph.py:215-225); written by ``csc_edgelist_write`` (Python's repr() of each weight)."""
+    indptr = np.ascontiguousarray(graph.indptr, dtype=np.int32)
+    indices = np.ascontiguousarray(graph.indices, dtype=np.int32)
+    weights = np.ascontiguousarray(graph.weights, dtype=np.float64)
+    _lib.call("csc_edgelist_write", str(Path(path)).encode(), int(graph.num_nodes), _lib.ptr(indptr),
+              _lib.ptr(indices), _lib.ptr(weights), 0)

@@ -8,7 +8,8 @@ not shipped to the GPU box):
 
 Outputs (committed, small): tests/golden/graphs.npz, filter_c1.npz,
 pipeline_c1.npz, formats.npz (the reference's own on-disk formats: feature dump,
-labels CSV, result JSON, dichotomy trace CSV) and, with --c2, pipeline_c2.npz
+labels CSV, result JSON, dichotomy trace CSV), edgelists.npz (read_edge_list on messy and
+failing files, write_edge_list bytes) and, with --c2, pipeline_c2.npz
 (scalars, indices and labels only; the reference takes ~2.5 min there).
 """
 
@@ -133,6 +134,79 @@ def formats():
                         provenance=np.frombuffer(json.dumps(prov).encode(), dtype=np.uint8))
 
 
+EDGE_TEXT = (
+    "# messy edge list: comments, blank lines, CRLF and lone CR, tabs, other ASCII whitespace\n"
+    "# nodes 12\n"
+    "0 1\n"
+    "\n"
+    "   \t\n"
+    "1\t2 0.5\r\n"
+    "2 3 1e-3\r"
+    "3 4 .5\n"
+    "4\x0b5\x0c5.\n"
+    "5 6 +2\n"
+    "6 7 1_000.5\n"
+    "1_0 11 3\n"
+    "007 8 2.25E+1\n"
+    "+8 9 0.1\n"
+    "9 \u0663 7\n"
+    "3\u00a010 1.5\n"
+    "#nodes 99 trailing tokens are not a header\n"
+    "# nodes +14\n"
+    "10 11 12345678901234567890.5\n"
+    "2 3 1e-3\n"
+    "  0 11   4  "
+)
+
+EDGE_ERRORS = {
+    "too_many": "0 1\n1 2 3 4\n",
+    "too_few": "# header\n0\n",
+    "bad_int": "0 1\n0 x 1.0\n",
+    "bad_float": "0 1 abc\n",
+    "bad_underscore": "1__0 2\n",
+    "self_loop": "0 0 1.0\n",
+}
+
+
+def edgelists():
+    """The reference's read_edge_list (graph.py:177-214) on a messy file and on failing files
+    (message with the path replaced by <path>), and write_edge_list's bytes (graph.py:215-225)
+    for a graph whose weights span many magnitudes."""
+    import tempfile
+
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        td = Path(td)
+        path = td / "messy.edges"
+        path.write_bytes(EDGE_TEXT.encode("utf-8"))
+        g = ref.read_edge_list(path)
+        out.update(messy_text=np.frombuffer(EDGE_TEXT.encode("utf-8"), dtype=np.uint8), messy_n=g.num_nodes,
+                   messy_indptr=g.indptr, messy_indices=g.indices, messy_weights=g.weights)
+        msgs = {}
+        for name, text in EDGE_ERRORS.items():
+            p = td / f"{name}.edges"
+            p.write_text(text)
+            try:
+                ref.read_edge_list(p)
+                msgs[name] = None
+            except Exception as exc:  # GraphError (ValueError)
+                msgs[name] = [type(exc).__name__, str(exc).replace(str(p), "<path>")]
+        out["error_texts"] = np.frombuffer(json.dumps(EDGE_ERRORS).encode(), dtype=np.uint8)
+        out["error_msgs"] = np.frombuffer(json.dumps(msgs).encode(), dtype=np.uint8)
+        rng = np.random.default_rng(31)
+        n, m = 60, 400
+        src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+        keep = src != dst
+        mags = 10.0 ** rng.uniform(-9, 21, m)
+        w = np.where(rng.random(m) < 0.3, np.round(mags), mags)
+        w[:6] = [1.0, 0.1, 1e16, 1e-5, 123456789012345678.0, 2.5e-7]
+        wg = ref.build_graph(np.column_stack([src[keep], dst[keep], w[keep]]), num_nodes=n + 3)
+        ref.write_edge_list(wg, td / "w.edges")
+        out.update(write_n=wg.num_nodes, write_indptr=wg.indptr, write_indices=wg.indices, write_weights=wg.weights,
+                   write_bytes=np.frombuffer((td / "w.edges").read_bytes(), dtype=np.uint8))
+    np.savez_compressed(OUT / "edgelists.npz", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
@@ -140,6 +214,7 @@ def main():
     graphs()
     filter_c1()
     formats()
+    edgelists()
     np.savez_compressed(OUT / "pipeline_c1.npz", **pipeline(1000, 20, int(math.ceil(4 * math.log(1000))), 0, True))
     if args.c2:
         np.savez_compressed(OUT / "pipeline_c2.npz", **pipeline(100_000, 20, int(math.ceil(4 * math.log(1e5))), 0, False))

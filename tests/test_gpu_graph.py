@@ -134,3 +134,42 @@ def test_edge_list_round_trip(tmp_path):
     (tmp_path / "bad.edges").write_text("0 1\nnonsense line here oops\n")
     with pytest.raises(P.GraphError, match=":2"):
         P.read_edge_list(tmp_path / "bad.edges")
+
+
+def test_read_edge_list_matches_reference(tmp_path):
+    """read_edge_list on the messy golden file: the reference's CSR, node count from the last
+    '# nodes' header; a self loop raises as in the reference (build_graph, self_loops='error')."""
+    import json
+
+    from conftest import golden
+
+    eg = golden("edgelists")
+    p = tmp_path / "messy.edges"
+    p.write_bytes(bytes(eg["messy_text"]))
+    g = P.read_edge_list(p)
+    assert g.num_nodes == int(eg["messy_n"])
+    assert np.array_equal(g.indptr, eg["messy_indptr"]) and np.array_equal(g.indices, eg["messy_indices"])
+    assert np.array_equal(g.weights, eg["messy_weights"])
+    msgs = json.loads(bytes(eg["error_msgs"]).decode())
+    q = tmp_path / "loop.edges"
+    q.write_text(json.loads(bytes(eg["error_texts"]).decode())["self_loop"])
+    with pytest.raises(P.GraphError, match=msgs["self_loop"][1]):
+        P.read_edge_list(q)
+
+
+def test_edge_list_round_trip_bit_identical(tmp_path):
+    """write_edge_list -> read_edge_list reproduces the CSR bit for bit (test_graph.py:146-162),
+    including trailing isolated nodes, and the file is the oracle's bytes."""
+    rng = np.random.default_rng(5)
+    n, m = 300, 2000
+    src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+    keep = src != dst
+    w = 10.0 ** rng.uniform(-6, 8, m)
+    g = P.build_graph(np.column_stack([src[keep], dst[keep], w[keep]]), num_nodes=n + 4)
+    path = tmp_path / "rt.edges"
+    P.write_edge_list(g, path)
+    assert path.read_bytes() == O.format_edge_list(g.num_nodes, g.indptr, g.indices, g.weights)
+    g2 = P.read_edge_list(path)
+    assert g2.num_nodes == n + 4
+    assert np.array_equal(g2.indptr, g.indptr) and np.array_equal(g2.indices, g.indices)
+    assert np.array_equal(g2.weights, g.weights)
