@@ -353,6 +353,109 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Lean mid step (the hot case: unit-weight graph, Clenshaw or first steps in the scaled
+// basis, no epilogue, no forward accumulator, no peer stores):
+//   out~_i = ka d_i^-1 sum_j G~_j + ks S~_i + kx X~_i
+// Same schedule and chunking as k_cheb_step, with only the state that case needs, so it
+// fits 32 registers and runs 64 warps per SM (8 CTAs of 256 threads).
+template <typename T, int LPR, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
+  using VT = Vec16<T>;
+  using V = typename VT::type;
+  using V2 = typename Pair<T>::type;
+  constexpr int VEC = VT::n;
+  constexpr int GPW = 32 / LPR;
+  constexpr int CH = LPR > 4 ? (LPR < 32 ? LPR : 8) : 4;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPR;
+  const int grp = lane / LPR;
+  const bool lane_on = sub * VEC < a.wc;
+  const int n = (int)a.n;
+  const int ngroups = (n + GPW - 1) / GPW;
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  const V* __restrict__ Gv = static_cast<const V*>(a.G) + sub;
+  const T ka = static_cast<T>(a.ka), ks = static_cast<T>(a.ks), kx = static_cast<T>(a.kx);
+  int gi = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int32_t nbeg = 0, nend = 0;
+  if (gi < ngroups && gi * GPW + grp < n) {
+    nbeg = __ldg(a.indptr + gi * GPW + grp);
+    nend = __ldg(a.indptr + gi * GPW + grp + 1);
+  }
+  for (; gi < ngroups; gi += nwarps) {
+    const int row = gi * GPW + grp;
+    const int cnt = nend - nbeg;
+    T acc[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) acc[c] = T(0);
+    {
+      const int maxcnt = __reduce_max_sync(FULL, cnt);
+      const int32_t* ip = a.indices + nbeg;
+      const bool own = CH >= LPR || sub < CH;  // this lane holds an index of each chunk
+      int32_t jj = (own && sub < cnt) ? __ldcs(ip + sub) : -1;
+      for (int base = 0; base < maxcnt; base += CH) {
+        const int e = base + CH + sub;
+        const int32_t jn = (own && base + CH < maxcnt && e < cnt) ? __ldcs(ip + e) : -1;
+        V gv[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int32_t j = LPR == 1 ? jj : __shfl_sync(FULL, jj, k % LPR, LPR);
+          gv[k] = VT::zero();
+          if (j >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)j * LPR);
+        }
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          T g[VEC];
+          VT::unpack(gv[k], g);
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) acc[c] += g[c];
+        }
+        jj = jn;
+      }
+    }
+    {  // next row group's indptr pair
+      const int nrow = (gi + nwarps) * GPW + grp;
+      if (gi + nwarps < ngroups && nrow < n) {
+        nbeg = __ldg(a.indptr + nrow);
+        nend = __ldg(a.indptr + nrow + 1);
+      } else {
+        nbeg = nend = 0;
+      }
+    }
+    if (row < n && lane_on) {
+      const uint32_t off = ((uint32_t)row * LPR + sub) * VEC;
+      const T si = static_cast<const V2*>(a.rs)[row].x;
+      const T kacc = ka * si * si;
+      T out[VEC], sv[VEC], xv[VEC];
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) sv[c] = xv[c] = T(0);
+      if (a.S) VT::unpack(__ldcs(reinterpret_cast<const V*>(static_cast<const T*>(a.S) + off)), sv);
+      if (a.X && a.kx != 0.0) VT::unpack(__ldcs(reinterpret_cast<const V*>(static_cast<const T*>(a.X) + off)), xv);
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) out[c] = fma(kx, xv[c], fma(ks, sv[c], kacc * acc[c]));
+      *reinterpret_cast<V*>(static_cast<T*>(a.O) + off) = VT::make(out);
+    }
+  }
+}
+
+template <typename T, int LPR>
+static int launch_mid(const StepArgs& a, int device, cudaStream_t s) {
+  auto kern = k_cheb_mid<T, LPR, 8>;
+  static int occ = 0;
+  if (occ == 0) {
+    int o = 0;
+    CSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, 0));
+    occ = std::max(o, 1);
+  }
+  const int64_t rows_per_block = 8 * (32 / LPR);
+  const int64_t need = (a.n + rows_per_block - 1) / rows_per_block;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)device_props(device).sms * occ));
+  kern<<<grid, 256, 0, s>>>(a);
+  CSC_LAUNCHED();
+  return grid;
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 template <typename T, int LPR, int EPI, int CHUNK, int MINB, bool UNIT>
 static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t s) {
@@ -470,6 +573,20 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   cudaEvent_t e0 = nullptr;
   if (prof) profile_begin(s, &e0);
   int grid = 0;
+  // Lean mid-step kernel (32 registers, 64 warps/SM) for the hot case: 128- and 256-B rows
+  // whose gather panel is at most 4x L2.  A/B on B200 (profiles/r01_panel_sweeps.txt): C3
+  // d=56 -1.7 %, CG k=100 -4.7 %, probe d=28 -5.8 %, fp64 d=56 -8.3 %; a 2 GB C5 panel
+  // (DRAM-bound random gathers) is 3.7 % slower with it, so large panels keep k_cheb_step.
+  const bool lean = g_opt.lean_mid.load() != 0 && epi == EPI_NONE && a.wv == nullptr && !a.fwd && !a.last &&
+                    a.npeers == 0 && a.G != nullptr && a.O != nullptr && !a.contig && threads == 256 &&
+                    g_opt.unroll.load() == 4 && g_opt.persistent.load() && persist_bytes(g->device) == 0 &&
+                    (lpr == 8 || lpr == 16) &&
+                    (double)a.n * lpr * 16.0 <= 4.0 * (double)device_props(g->device).l2_bytes;
+  if (lean) {
+    grid = lpr == 8 ? launch_mid<T, 8>(a, g->device, s) : launch_mid<T, 16>(a, g->device, s);
+    if (prof) profile_end(s, e0, step_bytes(g, a, epi));
+    return grid;
+  }
   switch (epi) {
     case EPI_NONE: grid = launch_epi<T, EPI_NONE>(a, lpr, threads, g->device, s); break;
     case EPI_SUMSQ: grid = launch_epi<T, EPI_SUMSQ>(a, lpr, threads, g->device, s); break;

@@ -164,6 +164,7 @@ static std::atomic<int64_t>* option_slot(const char* key) {
   if (k == "panel_width") return &g_opt.panel_width;
   if (k == "recurrence") return &g_opt.recurrence;
   if (k == "cache_hints") return &g_opt.cache_hints;
+  if (k == "lean_mid") return &g_opt.lean_mid;
   if (k == "block_threads") return &g_opt.block_threads;
   if (k == "profile") return &g_opt.profile;
   if (k == "l2_budget_pct") return &g_opt.l2_budget_pct;
@@ -187,6 +188,7 @@ int csc_set_option(const char* key, int64_t value) {
     if (k == "unroll" && value != 2 && value != 4 && value != 8) fail(CSC_ERR_INVALID, "unroll must be 2, 4 or 8");
     if (k == "l2_persist_pct" && (value < 0 || value > 100)) fail(CSC_ERR_INVALID, "l2_persist_pct in [0, 100]");
     if (k == "persistent" && value != 0 && value != 1) fail(CSC_ERR_INVALID, "persistent must be 0 or 1");
+    if (k == "lean_mid" && value != 0 && value != 1) fail(CSC_ERR_INVALID, "lean_mid must be 0 or 1");
     if (k == "l2_budget_pct" && (value < 1 || value > 100)) fail(CSC_ERR_INVALID, "l2_budget_pct in [1, 100]");
     slot->store(value);
   });

@@ -120,3 +120,21 @@ def test_dimension_mismatch():
     op = c1_op()
     with pytest.raises(ValueError):
         P.apply_filter(P.design_lowpass(1.0, 5), op, np.ones((5, 2)))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_lean_mid_step_kernel_matches_general_kernel(filter_golden, dtype):
+    """The 32-register mid-step kernel (k_cheb_mid, default for 128/256-B unit-weight rows)
+    gives the general step kernel's results bit for bit, for both recurrences and the panel
+    widths that route to it; and both match the reference."""
+    op = c1_op(dtype)
+    X = filter_golden["X"]
+    low = P.design_lowpass(0.37, 50)
+    for pw in (0, 8, 16, 32, 64):
+        for rec in (0, 1):
+            with options(panel_width=pw, recurrence=rec, lean_mid=0):
+                general = P.apply_filter(low, op, X)
+            with options(panel_width=pw, recurrence=rec, lean_mid=1):
+                lean = P.apply_filter(low, op, X)
+            assert np.array_equal(general, lean), (pw, rec)
+            assert relerr(lean, filter_golden["Y_low"]) <= (FP64_TOL if dtype == "float64" else FP32_TOL)
