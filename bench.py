@@ -15,6 +15,7 @@ Multi-GPU: one process per GPU (torchrun), graph replicated, each rank filters i
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -316,6 +317,8 @@ def run_ours(args, cfg):
         step_device()
     barrier()
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed regions (value and e2e); re-enabled below
     _lib.set_option("profile", 1)
     _lib.profile_reset()
     l0 = _lib.launch_count()
@@ -359,6 +362,7 @@ def run_ours(args, cfg):
         calls.append((time.perf_counter() - t1) * 1e3)  # step_e2e returns with the result on the host
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
+    gc.enable()
     # the host link this run saw (a slow or mis-placed box shows up here, not only in e2e)
     dev_t = torch.empty((N, d), dtype=torch.float64, device=f"cuda:{local}")
     link = {}

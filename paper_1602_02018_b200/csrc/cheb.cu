@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     if (row < n && lane_on) {
       const uint32_t off = ((uint32_t)row * LPR + sub) * VEC;
       const T si = static_cast<const V2*>(a.rs)[row].x;
-      const T kacc = ka * si * si;
+      const T kacc = ka * (si * si);  // as k_cheb_step (bit-identical results)
       T out[VEC], sv[VEC], xv[VEC];
 #pragma unroll
       for (int c = 0; c < VEC; ++c) sv[c] = xv[c] = T(0);
