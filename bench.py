@@ -401,7 +401,8 @@ def run_ours(args, cfg):
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-        "kernel": "k_cheb_step (fused Chebyshev step SpMM)", "peak_source": peak_src,
+        "kernel": "fused Chebyshev step SpMM: k_cheb_mid (mid steps) + k_cheb_step (first / last steps)",
+        "peak_source": peak_src,
         "kernel_ms_per_launch": step_ms / max(step_launches, 1), "launches_timed": step_launches,
         "algorithmic_bytes_per_launch": alg_per_step_set * args.steps / max(step_launches, 1),
         "algorithmic_unit": "SURVEY.md 8(d) B_step(d) = B_csr + 5 N d s per step launch (B_first on the first); "

@@ -365,7 +365,8 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
   using V2 = typename Pair<T>::type;
   constexpr int VEC = VT::n;
   constexpr int GPW = 32 / LPR;
-  constexpr int CH = LPR > 4 ? (LPR < 32 ? LPR : 8) : 4;
+  constexpr int CH = Rounds<LPR, 4>::CH;
+  constexpr int UC = Rounds<LPR, 4>::UC;  // indices held per lane per chunk
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int sub = lane % LPR;
@@ -391,15 +392,24 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     {
       const int maxcnt = __reduce_max_sync(FULL, cnt);
       const int32_t* ip = a.indices + nbeg;
-      const bool own = CH >= LPR || sub < CH;  // this lane holds an index of each chunk
-      int32_t jj = (own && sub < cnt) ? __ldcs(ip + sub) : -1;
+      int32_t jj[UC];
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {  // slot k of a chunk is entry k / LPR of lane k % LPR
+        const int e = u * LPR + sub;
+        jj[u] = (e < cnt && (UC > 1 || sub < CH)) ? __ldcs(ip + e) : -1;
+      }
       for (int base = 0; base < maxcnt; base += CH) {
-        const int e = base + CH + sub;
-        const int32_t jn = (own && base + CH < maxcnt && e < cnt) ? __ldcs(ip + e) : -1;
+        int32_t jn[UC];
+        const bool more = base + CH < maxcnt;  // warp-uniform
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+          const int e = base + CH + u * LPR + sub;
+          jn[u] = (more && e < cnt && (UC > 1 || sub < CH)) ? __ldcs(ip + e) : -1;
+        }
         V gv[CH];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
-          const int32_t j = LPR == 1 ? jj : __shfl_sync(FULL, jj, k % LPR, LPR);
+          const int32_t j = LPR == 1 ? jj[k] : __shfl_sync(FULL, jj[k / LPR], k % LPR, LPR);
           gv[k] = VT::zero();
           if (j >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)j * LPR);
         }
@@ -410,7 +420,8 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
 #pragma unroll
           for (int c = 0; c < VEC; ++c) acc[c] += g[c];
         }
-        jj = jn;
+#pragma unroll
+        for (int u = 0; u < UC; ++u) jj[u] = jn[u];
       }
     }
     {  // next row group's indptr pair
@@ -573,17 +584,23 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   cudaEvent_t e0 = nullptr;
   if (prof) profile_begin(s, &e0);
   int grid = 0;
-  // Lean mid-step kernel (32 registers, 64 warps/SM) for the hot case: 128- and 256-B rows
-  // whose gather panel is at most 4x L2.  A/B on B200 (profiles/r01_panel_sweeps.txt): C3
-  // d=56 -1.7 %, CG k=100 -4.7 %, probe d=28 -5.8 %, fp64 d=56 -8.3 %; a 2 GB C5 panel
-  // (DRAM-bound random gathers) is 3.7 % slower with it, so large panels keep k_cheb_step.
+  // Lean mid-step kernel (32 registers, 64 warps/SM) for the hot case: 16-, 64-, 128- and 256-B
+  // rows whose gather panel is at most 4x L2.  A/B on B200 (profiles/r01_panel_sweeps.txt): C3
+  // d=56 -1.7 %, CG k=100 -4.7 %, probe d=28 -5.8 %, fp64 d=56 -8.3 %, 16-B rows -4.3 %, 64-B
+  // rows -4.6 %; 32-B rows are 3 % slower and a 2 GB C5 panel (DRAM-bound random gathers)
+  // 3.7 % slower with it, so those keep k_cheb_step.
   const bool lean = g_opt.lean_mid.load() != 0 && epi == EPI_NONE && a.wv == nullptr && !a.fwd && !a.last &&
                     a.npeers == 0 && a.G != nullptr && a.O != nullptr && !a.contig && threads == 256 &&
                     g_opt.unroll.load() == 4 && g_opt.persistent.load() && persist_bytes(g->device) == 0 &&
-                    (lpr == 8 || lpr == 16) &&
+                    (lpr == 1 || lpr == 4 || lpr == 8 || lpr == 16) &&
                     (double)a.n * lpr * 16.0 <= 4.0 * (double)device_props(g->device).l2_bytes;
   if (lean) {
-    grid = lpr == 8 ? launch_mid<T, 8>(a, g->device, s) : launch_mid<T, 16>(a, g->device, s);
+    switch (lpr) {
+      case 1: grid = launch_mid<T, 1>(a, g->device, s); break;
+      case 4: grid = launch_mid<T, 4>(a, g->device, s); break;
+      case 8: grid = launch_mid<T, 8>(a, g->device, s); break;
+      default: grid = launch_mid<T, 16>(a, g->device, s); break;
+    }
     if (prof) profile_end(s, e0, step_bytes(g, a, epi));
     return grid;
   }
