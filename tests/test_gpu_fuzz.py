@@ -89,3 +89,40 @@ def test_wide_panels_heavy_weighted_rows(dtype, pw, rec, tol):
     finally:
         P._lib.set_option("panel_width", old_pw)
         P._lib.set_option("recurrence", old_rec)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_lean_kernel_unit_weights_isolated_and_heavy_rows(dtype):
+    """Unit-weight graph (the lean mid-step kernel's case) with isolated nodes and degrees from
+    0 to ~90: every panel width that routes to k_cheb_mid (16- to 512-B rows) and the 32-B rows
+    that do not, bit-identical to the general kernel and within tolerance of the oracle."""
+    rng = np.random.default_rng(23)
+    n = 900
+    deg = np.minimum(rng.pareto(1.3, n) * 5 + 1, 80).astype(int)
+    deg[rng.choice(n, 40, replace=False)] = 0
+    src = np.repeat(np.arange(n), deg)
+    dst = rng.integers(0, n - 30, src.size)  # the last 30 nodes only get edges from their own rows
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    ref = O.build_csr(src, dst, np.ones(src.size), n)
+    g = P.build_graph(np.column_stack([src, dst, np.ones(src.size)]), num_nodes=n)
+    assert (np.diff(ref.indptr) == 0).any() and np.diff(ref.indptr).max() > 64
+    op = P.laplacian_op(g, dtype=dtype)
+    filt = P.design_lowpass(0.55, 25)
+    tol = 1e-12 if dtype == "float64" else 1e-4
+    vec = 2 if dtype == "float64" else 4
+    old = {k: P._lib.get_option(k) for k in ("panel_width", "lean_mid")}
+    try:
+        for pw in (vec, 2 * vec, 4 * vec, 8 * vec, 16 * vec, 32 * vec):
+            X = rng.standard_normal((n, pw - 1 if pw > 1 else 1))
+            want = O.apply_filter(filt.coeffs, ref, X)
+            P._lib.set_option("panel_width", pw)
+            P._lib.set_option("lean_mid", 0)
+            general = P.apply_filter(filt, op, X)
+            P._lib.set_option("lean_mid", 1)
+            lean = P.apply_filter(filt, op, X)
+            assert np.array_equal(general, lean), pw
+            assert relerr(lean, want) <= tol, pw
+    finally:
+        for k, v in old.items():
+            P._lib.set_option(k, v)
