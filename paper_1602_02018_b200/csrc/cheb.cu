@@ -969,6 +969,95 @@ __global__ void k_normalize_rows(const T* __restrict__ Yp, const double* __restr
   }
 }
 
+// Single-panel features (the whole block in one panel, e.g. C3's d = 56 in one 64-wide
+// panel): LPR lanes per row move 16-byte vectors, several rows per warp, stores vectorised;
+// same arithmetic as k_normalize_rows (fp64 v / ||row||, features.py:84-87).
+template <typename T, typename To, int LPR>
+__global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, int wc, const double* __restrict__ rowsq,
+                                                      int64_t n, To* __restrict__ F, int64_t ldf,
+                                                      uint8_t* __restrict__ zflag,
+                                                      unsigned long long* __restrict__ nzero) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  constexpr int PW = LPR * VEC;
+  constexpr int GPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, sub = lane % LPR, grp = lane / LPR;
+  const int col0 = sub * VEC;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned zeros = 0;
+  for (int64_t row = warp * GPW + grp; row - grp < n; row += nw * GPW) {
+    if (row < n) {
+      T v[VEC];
+      if (col0 < wc) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 q = __ldcs(reinterpret_cast<const float4*>(Yp + row * PW + col0));
+          v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+        } else {
+          const double2 q = __ldcs(reinterpret_cast<const double2*>(Yp + row * PW + col0));
+          v[0] = q.x, v[1] = q.y;
+        }
+      }
+      const double nrm = sqrt(rowsq[row]);
+      const bool zero = nrm <= 1e-300;  // features.py:23, 81
+      if (col0 < wc) {
+        To o[VEC];
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) o[c] = zero ? To(0) : static_cast<To>((double)v[c] / nrm);
+        To* dst = F + row * ldf + col0;
+        if (col0 + VEC <= wc) {  // 16-B aligned: ldf * sizeof(To) and col0 * sizeof(To) are multiples of 16
+          if constexpr (sizeof(To) == 4 && VEC == 4) {
+            __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
+          } else if constexpr (sizeof(To) == 8 && VEC == 4) {
+            __stcs(reinterpret_cast<double2*>(dst), make_double2(o[0], o[1]));
+            __stcs(reinterpret_cast<double2*>(dst) + 1, make_double2(o[2], o[3]));
+          } else if constexpr (sizeof(To) == 8 && VEC == 2) {
+            __stcs(reinterpret_cast<double2*>(dst), make_double2(o[0], o[1]));
+          } else {
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) dst[c] = o[c];
+          }
+        } else {
+          for (int c = 0; c < wc - col0; ++c) dst[c] = o[c];
+        }
+      }
+      if (sub == 0) {
+        if (zflag) zflag[row] = zero ? 1 : 0;
+        zeros += zero ? 1u : 0u;
+      }
+    }
+  }
+  if (zeros) atomicAdd(nzero, (unsigned long long)zeros);
+}
+
+template <typename T, typename To>
+static bool launch_normalize_1p(const PanelPlan& pp, const T* Yp, const double* rowsq, int64_t n, To* F, int64_t ldf,
+                                uint8_t* zflag, unsigned long long* nzero, int device, cudaStream_t s) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  if (pp.np != 1 || ((size_t)ldf * sizeof(To)) % 16 != 0 || reinterpret_cast<uintptr_t>(F) % 16 != 0) return false;
+  if ((VEC * sizeof(To)) % 16 != 0 && VEC * sizeof(To) != 8) return false;
+  const int lpr = pp.pw[0] / VEC;
+  const int64_t rows_per_block = 8 * (32 / lpr);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + rows_per_block - 1) / rows_per_block,
+                                                               (int64_t)device_props(device).sms * 8));
+  switch (lpr) {
+#define CSC_NORM1P(L)                                                                                        \
+  case L:                                                                                                    \
+    k_normalize_1p<T, To, L><<<grid, 256, 0, s>>>(Yp, pp.wc[0], rowsq, n, F, ldf, zflag, nzero);             \
+    break;
+    CSC_NORM1P(1)
+    CSC_NORM1P(2)
+    CSC_NORM1P(4)
+    CSC_NORM1P(8)
+    CSC_NORM1P(16)
+    CSC_NORM1P(32)
+#undef CSC_NORM1P
+    default:
+      return false;
+  }
+  CSC_LAUNCHED();
+  return true;
+}
+
 __global__ void k_sum_panels(const double* __restrict__ rowsq, int np, int64_t n, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double t = 0.0;
@@ -1358,7 +1447,23 @@ int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, co
     const int* wc = pw + pp.np;
     const int* c0 = pw + 2 * pp.np;
     const int grid = (int)std::min<int64_t>((n + 7) / 8, (int64_t)device_props(g->device).sms * 16);
-    if (g->dtype == CSC_F64 && io_dtype == CSC_F64)
+    bool done = false;
+    if (g_opt.fast_normalize.load()) {
+      if (g->dtype == CSC_F64 && io_dtype == CSC_F64)
+        done = launch_normalize_1p<double, double>(pp, yp.as<double>(), rowsq.as<double>(), n, (double*)fo.p, fo.ld,
+                                                   zo.as<uint8_t>(), nz.as<unsigned long long>(), g->device, s);
+      else if (g->dtype == CSC_F32 && io_dtype == CSC_F64)
+        done = launch_normalize_1p<float, double>(pp, yp.as<float>(), rowsq.as<double>(), n, (double*)fo.p, fo.ld,
+                                                  zo.as<uint8_t>(), nz.as<unsigned long long>(), g->device, s);
+      else if (g->dtype == CSC_F64 && io_dtype == CSC_F32)
+        done = launch_normalize_1p<double, float>(pp, yp.as<double>(), rowsq.as<double>(), n, (float*)fo.p, fo.ld,
+                                                  zo.as<uint8_t>(), nz.as<unsigned long long>(), g->device, s);
+      else
+        done = launch_normalize_1p<float, float>(pp, yp.as<float>(), rowsq.as<double>(), n, (float*)fo.p, fo.ld,
+                                                 zo.as<uint8_t>(), nz.as<unsigned long long>(), g->device, s);
+    }
+    if (done) {
+    } else if (g->dtype == CSC_F64 && io_dtype == CSC_F64)
       k_normalize_rows<double, double><<<grid, 256, 0, s>>>(yp.as<double>(), rowsq.as<double>(), pp.np, pw, wc, c0,
                                                             doff.as<int64_t>(), n, (double*)fo.p, fo.ld,
                                                             zo.as<uint8_t>(), nz.as<unsigned long long>());
@@ -1374,7 +1479,7 @@ int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, co
       k_normalize_rows<float, float><<<grid, 256, 0, s>>>(yp.as<float>(), rowsq.as<double>(), pp.np, pw, wc, c0,
                                                           doff.as<int64_t>(), n, (float*)fo.p, fo.ld,
                                                           zo.as<uint8_t>(), nz.as<unsigned long long>());
-    CSC_LAUNCHED();
+    if (!done) CSC_LAUNCHED();
     finish_out(fo, n, ncols, io_dtype, s);
     zo.finish();
     unsigned long long hz = 0;

@@ -261,3 +261,35 @@ def test_block_cg_column_compaction_is_exact(c1_golden, dtype, tol):
     assert np.array_equal(ia.iterations, ib.iterations) and np.array_equal(ia.converged, ib.converged)
     assert relerr(Xb, Xa) <= tol
     assert len(set(ia.iterations.tolist())) > 1  # staggered convergence: compaction actually happened
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_fast_single_panel_normalisation_bit_identical(c1_golden, dtype):
+    """The vectorised single-panel normaliser (default) and the general one give the same bytes,
+    zero rows and flags included (isolated nodes whose signal rows are zero), for host fp64 and
+    device outputs of the compute dtype, at widths that fill a panel exactly and partially."""
+    import torch
+
+    g, _ = c1_graph()
+    src, dst = np.repeat(np.arange(g.num_nodes), np.diff(g.indptr)), g.indices
+    gi = P.build_graph(np.column_stack([src, dst, g.weights]), num_nodes=g.num_nodes + 5)  # 5 isolated nodes
+    op = P.laplacian_op(gi, dtype=dtype)
+    low = P.design_lowpass(0.4, 30)
+    rng = np.random.default_rng(9)
+    for w in (3, 16, 28, 31, 64 if dtype == "float32" else 32):
+        X = rng.standard_normal((gi.num_nodes, w))
+        X[-5:-2] = 0.0
+        out = {}
+        for fast in (0, 1):
+            with options(fast_normalize=fast):
+                F = np.empty_like(X)
+                z = P.features.features_into(op, low, X, F)
+                Xd = torch.tensor(X, device="cuda", dtype=torch.float32 if dtype == "float32" else torch.float64)
+                Fd = torch.empty_like(Xd)
+                zd = P.features.features_into(op, low, Xd, Fd)
+                out[fast] = (F, z, Fd.cpu().numpy(), zd)
+        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][2], out[1][2]), w
+        assert out[0][1].tolist() == out[1][1].tolist() == out[0][3].tolist() == out[1][3].tolist() == [
+            gi.num_nodes - 5, gi.num_nodes - 4, gi.num_nodes - 3], w
+        rows, zero = O.build_features(low.coeffs, O.Csr(gi.num_nodes, gi.indptr, gi.indices, gi.weights, gi.degrees), X)
+        assert relerr(out[1][0], rows) <= (1e-9 if dtype == "float64" else 1e-4), w
