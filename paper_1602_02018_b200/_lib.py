@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 from pathlib import Path
 
@@ -125,7 +126,17 @@ def check(status: int) -> None:
 
 
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args))
+    status = getattr(load(), name)(*args)
+    if status == CSC_ERR_NOMEM and "torch" in sys.modules:
+        # the library already handed its own pool's cached blocks back; torch's caching
+        # allocator may hold the rest.  Entry points are pure (outputs fully rewritten), so
+        # one retry after emptying torch's cache is safe.
+        import torch
+
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+            status = getattr(load(), name)(*args)
+    check(status)
 
 
 def ptr(a) -> int | None:

@@ -115,6 +115,10 @@ const DeviceProps& device_props(int dev);
 void ensure_pool(int dev);  // keep freed stream-ordered memory cached
 
 // Stream-ordered scratch allocation, freed on the same stream at scope exit.
+// Synchronise the current device and release the memory its stream-ordered pools cache
+// (the default pool and the side pool) back to the driver.  Used when an allocation fails.
+void trim_pools();
+
 class Scratch {
  public:
   Scratch() = default;
@@ -129,10 +133,18 @@ class Scratch {
     release();
     s_ = s;
     if (bytes == 0) bytes = 16;
-    if (pool)
-      CSC_CUDA(cudaMallocFromPoolAsync(&p_, bytes, pool, s));
-    else
-      CSC_CUDA(cudaMallocAsync(&p_, bytes, s));
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(&p_, bytes, pool, s) : cudaMallocAsync(&p_, bytes, s);
+    if (e == cudaErrorMemoryAllocation) {  // hand the pools' cached free blocks back, retry once
+      cudaGetLastError();
+      trim_pools();
+      e = pool ? cudaMallocFromPoolAsync(&p_, bytes, pool, s) : cudaMallocAsync(&p_, bytes, s);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p_ = nullptr;
+      fail(e == cudaErrorMemoryAllocation ? CSC_ERR_NOMEM : CSC_ERR_CUDA,
+           std::string("cudaMallocAsync(&p_, bytes, s) failed: ") + cudaGetErrorString(e));
+    }
     bytes_ = bytes;
   }
   void release() {

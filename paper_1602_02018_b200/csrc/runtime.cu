@@ -125,6 +125,16 @@ cudaMemPool_t side_pool(int dev) {
   return pools[dev];
 }
 
+void trim_pools() {
+  int dev = 0;
+  CSC_CUDA(cudaGetDevice(&dev));
+  CSC_CUDA(cudaDeviceSynchronize());
+  cudaMemPool_t pool;
+  CSC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  CSC_CUDA(cudaMemPoolTrimTo(pool, 0));
+  CSC_CUDA(cudaMemPoolTrimTo(side_pool(dev), 0));
+}
+
 bool is_device_ptr(const void* p, int device) {
   cudaPointerAttributes a;
   cudaError_t e = cudaPointerGetAttributes(&a, p);

@@ -25,7 +25,10 @@ cfg = CONFIGS[args.config]
 g, truth = make_graph(P, cfg)
 op = P.laplacian_op(g, dtype=args.dtype or cfg["dtype"])
 d = int(math.ceil(4 * math.log(cfg["N"])))
+res = None
 for r in range(args.reps):
+    del res  # the previous result's N x k soft indicators (64 GB at C5) must not outlive the next call
+    res = None
     t0 = time.perf_counter()
     res = P.run_csc(op, P.CscParams(k=cfg["k"], d=d, seed=0))
     wall = time.perf_counter() - t0
