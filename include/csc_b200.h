@@ -71,8 +71,9 @@ int csc_launch_count(int64_t* out);
  *   "unroll"        neighbour gathers in flight per lane / occupancy: 4 (default: 4 in
  *                   flight, 6 CTAs/SM), 2 (4 in flight, 8 CTAs/SM), 8 (8 in flight, 2 CTAs/SM)
  *   "row_order"     0 interleaved row groups (default), 1 contiguous runs per warp
- *   "lean_mid"      1 (default): 32-register mid-step kernel for unit-weight 16/64/128/256/512-B panel
- *                   rows whose gather panel is <= 4x L2; 0: always the general step kernel
+ *   "lean_mid"      1 (default): lean mid-step kernel for 16/64/128/256/512-B panel rows whose
+ *                   gather panel is <= 4x L2 (unit weights; weighted graphs in fp32);
+ *                   0: always the general step kernel
  *   "l2_budget_pct" L2 share a gathered panel may use (auto panel width)
  *   "l2_persist_pct" >0: persisting-L2 access window on the gathered panel
  *   "profile"       1 = time the Chebyshev step kernels with CUDA events            */

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 // Same schedule and chunking as k_cheb_step, with only the state that case needs, so it
 // fits 32 registers and runs 64 warps per SM (8 CTAs of 256 threads); 256-B rows use the
 // 40-register / 6-CTA build (five gathers in flight per lane).
-template <typename T, int LPR, int MINB>
+template <typename T, int LPR, int MINB, bool UNIT>
 __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
   using VT = Vec16<T>;
   using V = typename VT::type;
@@ -393,24 +393,33 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     {
       const int maxcnt = __reduce_max_sync(FULL, cnt);
       const int32_t* ip = a.indices + nbeg;
+      const T* wp = static_cast<const T*>(a.wv) + nbeg;  // edge weights (weighted graphs only)
       int32_t jj[UC];
+      T ww[UC];
 #pragma unroll
       for (int u = 0; u < UC; ++u) {  // slot k of a chunk is entry k / LPR of lane k % LPR
         const int e = u * LPR + sub;
-        jj[u] = (e < cnt && (UC > 1 || sub < CH)) ? __ldcs(ip + e) : -1;
+        const bool ok = e < cnt && (UC > 1 || sub < CH);
+        jj[u] = ok ? __ldcs(ip + e) : -1;
+        if constexpr (!UNIT) ww[u] = ok ? __ldcs(wp + e) : T(0);
       }
       for (int base = 0; base < maxcnt; base += CH) {
         int32_t jn[UC];
+        T wn[UC];
         const bool more = base + CH < maxcnt;  // warp-uniform
 #pragma unroll
         for (int u = 0; u < UC; ++u) {
           const int e = base + CH + u * LPR + sub;
-          jn[u] = (more && e < cnt && (UC > 1 || sub < CH)) ? __ldcs(ip + e) : -1;
+          const bool ok = more && e < cnt && (UC > 1 || sub < CH);
+          jn[u] = ok ? __ldcs(ip + e) : -1;
+          if constexpr (!UNIT) wn[u] = ok ? __ldcs(wp + e) : T(0);
         }
         V gv[CH];
+        T wk[CH];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
           const int32_t j = LPR == 1 ? jj[k] : __shfl_sync(FULL, jj[k / LPR], k % LPR, LPR);
+          if constexpr (!UNIT) wk[k] = LPR == 1 ? ww[k] : __shfl_sync(FULL, ww[k / LPR], k % LPR, LPR);
           gv[k] = VT::zero();
           if (j >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)j * LPR);
         }
@@ -419,10 +428,18 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
           T g[VEC];
           VT::unpack(gv[k], g);
 #pragma unroll
-          for (int c = 0; c < VEC; ++c) acc[c] += g[c];
+          for (int c = 0; c < VEC; ++c) {
+            if constexpr (UNIT)
+              acc[c] += g[c];
+            else
+              acc[c] = fma(wk[k], g[c], acc[c]);  // as k_cheb_step
+          }
         }
 #pragma unroll
-        for (int u = 0; u < UC; ++u) jj[u] = jn[u];
+        for (int u = 0; u < UC; ++u) {
+          jj[u] = jn[u];
+          if constexpr (!UNIT) ww[u] = wn[u];
+        }
       }
     }
     {  // next row group's indptr pair
@@ -454,8 +471,10 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
 // than 8 CTAs at 32; narrower rows prefer 8 CTAs (1 % the other way)
 template <typename T, int LPR, int MINB = (LPR == 16 ? 6 : 8)>
 static int launch_mid(const StepArgs& a, int device, cudaStream_t s) {
-  auto kern = k_cheb_mid<T, LPR, MINB>;
-  static int occ = 0;
+  const bool unit = a.wv == nullptr;
+  auto kern = unit ? k_cheb_mid<T, LPR, MINB, true> : k_cheb_mid<T, LPR, MINB, false>;
+  static int occ_cache[2] = {0, 0};  // [unit]
+  int& occ = occ_cache[unit ? 1 : 0];
   if (occ == 0) {
     int o = 0;
     CSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, 0));
@@ -592,7 +611,9 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   // C3 d=56 -1.7 %, CG k=100 -4.7 %, probe d=28 -5.8 %, fp64 d=56 -8.3 %, 16-B rows -4.3 %, 64-B
   // rows -4.6 %, 512-B rows -4.5 % (C4 k=250) to -20 % (C2 fp64); 32-B rows are 3 % slower and
   // a 2 GB C5 panel (DRAM-bound random gathers) 3.7 % slower with it: those keep k_cheb_step.
-  const bool lean = g_opt.lean_mid.load() != 0 && epi == EPI_NONE && a.wv == nullptr && !a.fwd && !a.last &&
+  // Weighted graphs: fp32 -3.5 to -5 %, fp64 +5 % (weights cost the fp64 build its buffers).
+  const bool lean = g_opt.lean_mid.load() != 0 && epi == EPI_NONE && (a.wv == nullptr || sizeof(T) == 4) &&
+                    !a.fwd && !a.last &&
                     a.npeers == 0 && a.G != nullptr && a.O != nullptr && !a.contig && threads == 256 &&
                     g_opt.unroll.load() == 4 && g_opt.persistent.load() && persist_bytes(g->device) == 0 &&
                     lpr != 2 &&

@@ -91,8 +91,9 @@ def test_wide_panels_heavy_weighted_rows(dtype, pw, rec, tol):
         P._lib.set_option("recurrence", old_rec)
 
 
+@pytest.mark.parametrize("weighted", [False, True])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-def test_lean_kernel_unit_weights_isolated_and_heavy_rows(dtype):
+def test_lean_kernel_unit_weights_isolated_and_heavy_rows(dtype, weighted):
     """Unit-weight graph (the lean mid-step kernel's case) with isolated nodes and degrees from
     0 to ~90: every panel width that routes to k_cheb_mid (16- to 512-B rows) and the 32-B rows
     that do not, bit-identical to the general kernel and within tolerance of the oracle."""
@@ -104,8 +105,9 @@ def test_lean_kernel_unit_weights_isolated_and_heavy_rows(dtype):
     dst = rng.integers(0, n - 30, src.size)  # the last 30 nodes only get edges from their own rows
     keep = src != dst
     src, dst = src[keep], dst[keep]
-    ref = O.build_csr(src, dst, np.ones(src.size), n)
-    g = P.build_graph(np.column_stack([src, dst, np.ones(src.size)]), num_nodes=n)
+    w = rng.choice([0.5, 1.0, 2.25, 3.0], src.size) if weighted else np.ones(src.size)
+    ref = O.build_csr(src, dst, w, n)
+    g = P.build_graph(np.column_stack([src, dst, w]), num_nodes=n)
     assert (np.diff(ref.indptr) == 0).any() and np.diff(ref.indptr).max() > 64
     op = P.laplacian_op(g, dtype=dtype)
     filt = P.design_lowpass(0.55, 25)

@@ -39,6 +39,12 @@ dtype = {dtype!r} or cfg["dtype"]
 N = cfg["N"]
 d = {width} or int(math.ceil(4 * math.log(N)))
 g, _ = make_graph(P, cfg)
+if {weighted}:  # same edges, weights drawn from {{0.5, 1, 2.25, 3}} (symmetric: drawn per i < j edge)
+    import numpy as np
+    rows = np.repeat(np.arange(g.num_nodes), np.diff(g.indptr))
+    keep = rows < g.indices
+    w = np.random.default_rng(1).choice([0.5, 1.0, 2.25, 3.0], int(keep.sum()))
+    g = P.build_graph(np.column_stack([rows[keep], g.indices[keep], w]), num_nodes=g.num_nodes)
 op = P.laplacian_op(g, dtype=dtype)
 tdt = torch.float32 if dtype == "float32" else torch.float64
 X = torch.randn(N, d, dtype=torch.float64, device="cuda").div_(math.sqrt(d)).to(tdt)
@@ -69,6 +75,7 @@ def main():
     ap.add_argument("--dtype", default="")
     ap.add_argument("--rounds", type=int, default=6)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--weighted", action="store_true", help="random edge weights on the config's graph")
     args = ap.parse_args()
     libs = {"A": str(Path(args.lib_a).resolve()), "B": str(Path(args.lib_b).resolve())}
     opts = {"A": args.opts_a, "B": args.opts_b}
@@ -76,7 +83,7 @@ def main():
     for r in range(args.rounds):
         for tag in ("A", "B") if r % 2 == 0 else ("B", "A"):
             code = CHILD.format(root=str(ROOT), lib=libs[tag], opts=opts[tag], config=args.config, dtype=args.dtype,
-                                width=args.width, reps=args.reps)
+                                width=args.width, reps=args.reps, weighted=bool(args.weighted))
             out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=os.environ,
                                  cwd=str(ROOT))
             if out.returncode != 0:
