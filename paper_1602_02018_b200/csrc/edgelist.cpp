@@ -340,7 +340,7 @@ extern "C" int csc_edgelist_write(const char* path, int64_t num_nodes, const int
     auto fmt = [&](int t) {
       const int64_t r0 = num_nodes * t / T, r1 = num_nodes * (t + 1) / T;
       std::string& s = part[t];
-      s.reserve((size_t)std::max<int64_t>(0, indptr[r1] - indptr[r0]) * 14);
+      if (r1 > r0) s.reserve((size_t)std::max<int64_t>(0, indptr[r1] - indptr[r0]) * 14);
       char line[96];
       for (int64_t i = r0; i < r1; ++i)
         for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) {

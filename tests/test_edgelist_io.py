@@ -159,3 +159,13 @@ def test_parallel_chunks_match_oracle(tmp_path):
     rows, hdr = G.parse_edge_list(p)
     want, whdr = O.parse_edge_text(text)
     assert hdr == whdr == 10001 and np.array_equal(rows, want)
+
+
+def test_writer_empty_graph_and_null_arrays(tmp_path):
+    p = tmp_path / "e.edges"
+    _lib.call("csc_edgelist_write", str(p).encode(), 0, None, None, None, 0)
+    assert p.read_bytes() == O.format_edge_list(0, [0], [], [])
+    with pytest.raises(ValueError):
+        _lib.call("csc_edgelist_write", str(p).encode(), 3, None, None, None, 0)
+    with pytest.raises(ValueError):
+        _lib.call("csc_edgelist_read", str(tmp_path / "missing.edges").encode(), 0, C.byref(C.c_void_p()))
