@@ -68,6 +68,16 @@ def _ncu_dram_pct(config: str, dtype: str):
     return json.loads(tf.read_text()).get(f"{config}_{dtype}_dram_throughput_pct")
 
 
+def _ncu_dram_gbs(config: str, dtype: str):
+    """DRAM bytes per K2 launch / its ncu duration (dram__bytes.sum.per_second), same capture."""
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if not tf.exists():
+        return None
+    d = json.loads(tf.read_text())
+    b, us = d.get(f"{config}_{dtype}"), d.get("duration_us")
+    return b / (sum(us) / len(us) * 1e-6) / 1e9 if b and us else None
+
+
 def peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -410,11 +420,13 @@ def run_ours(args, cfg):
         "kernel_stream_bytes_per_launch": step_bytes / max(step_launches, 1),
         "frac_of_8tbs": (achieved / 8000.0) if achieved else None,  # report against both peaks
         "ncu_dram_throughput_pct": _ncu_dram_pct(args.config, cfg["dtype"]),
+        "ncu_dram_gbs": _ncu_dram_gbs(args.config, cfg["dtype"]),
         "kernel_share_of_step": (step_ms / args.steps) / ms if ms > 0 else None,
         "recurrence": "clenshaw" if _lib.get_option("recurrence") == 0 else "forward",
-        # K2 is bound by the neighbour-gather traffic through L2 (deg x row bytes per step), not by
-        # DRAM: the gathered panel is L2-resident.  Measured ceiling for random 64-byte row gathers
-        # on this GPU: tools/microbench/gather_bench.cu (LDG, 64 warps/SM).
+        # Every step re-reads each gathered row ~deg times through L2 (L2->SM bytes below); at C3
+        # the 256 MB gather panel exceeds L2 and the random inter-community gathers come from
+        # DRAM.  The gathers alone take 253-302 us per step on this graph
+        # (profiles/r01_gather_sol.txt); the 64-B-row L2 ceiling is kept for reference.
         "l2_path": {
             "bytes_per_filter": (step_bytes / args.steps + P_ORDER * (nnz - N) * d * (4 if cfg["dtype"] == "float32" else 8)),
             "achieved_gbs": ((step_bytes / args.steps + P_ORDER * (nnz - N) * d * (4 if cfg["dtype"] == "float32" else 8))
@@ -423,6 +435,10 @@ def run_ours(args, cfg):
             "ceiling_source": "random 64-B row gathers, LDG at 64 warps/SM: tools/microbench/gather_bench.cu",
             "note": "L2->SM bytes = algorithmic bytes + (deg-1) extra reads of every gathered row per step",
         },
+        "gather_sol_us_per_step": ({"warps_48": 302.0, "warps_64": 253.0,
+                                    "source": "one step's neighbour-row gathers alone on the C3 graph "
+                                              "(tools/microbench/csr_gather_sol.cu, profiles/r01_gather_sol.txt)"}
+                                   if args.config == "c3" and cfg["dtype"] == "float32" else None),
     }
     cpub = None
     if world == 1 and not args.no_cpu:
