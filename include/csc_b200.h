@@ -76,6 +76,8 @@ int csc_launch_count(int64_t* out);
  *                   0: always the general step kernel
  *   "l2_budget_pct" L2 share a gathered panel may use (auto panel width)
  *   "l2_persist_pct" >0: persisting-L2 access window on the gathered panel
+ *   "cg_compact"    1 (default): block CG moves still-active columns into narrower panels
+ *   "cg_overlap"    1 (default): a narrower remainder CG panel runs on a side stream / host thread
  *   "profile"       1 = time the Chebyshev step kernels with CUDA events            */
 int csc_set_option(const char* key, int64_t value);
 int csc_get_option(const char* key, int64_t* value);

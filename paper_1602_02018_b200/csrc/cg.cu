@@ -15,7 +15,12 @@
 // partials, beta + freeze bookkeeping, and P = R + beta P.
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <future>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "filter.cuh"
@@ -402,6 +407,50 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
 }  // namespace
 }  // namespace csc
 
+namespace csc {
+namespace {
+// One persistent host thread that runs a narrow remainder panel's CG beside the main
+// panels (its pinned per-thread staging in cg_panel is allocated once, like the caller's).
+// Leaked on purpose: joining at process exit would race the CUDA runtime's teardown.
+class SideWorker {
+ public:
+  static SideWorker& get() {
+    static SideWorker* w = new SideWorker();
+    return *w;
+  }
+  std::future<void> submit(std::function<void()> fn) {
+    std::packaged_task<void()> task(std::move(fn));
+    std::future<void> fut = task.get_future();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.push_back(std::move(task));
+    }
+    cv_.notify_one();
+    return fut;
+  }
+
+ private:
+  SideWorker() : th_([this] { loop(); }) { th_.detach(); }
+  void loop() {
+    for (;;) {
+      std::packaged_task<void()> task;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return !q_.empty(); });
+        task = std::move(q_.front());
+        q_.pop_front();
+      }
+      task();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::packaged_task<void()>> q_;
+  std::thread th_;
+};
+}  // namespace
+}  // namespace csc
+
 using namespace csc;
 
 extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int ncoeffs, double gamma, double ridge,
@@ -455,15 +504,55 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
 
     Scratch xp(cs * std::max<int64_t>(pp.total, 1), s);
     int64_t run = 0;
-    for (int j = 0; j < pp.np; ++j) {
+    auto panel = [&](int j, int64_t* runp, cudaStream_t st) {
       if (g->dtype == CSC_F64)
         cg_panel<double>(g, hp_coeffs, ncoeffs, gamma, ridge, mask.as<uint8_t>(), didx.as<int64_t>(), n,
                          dred.as<double>(), k, tol, max_iters, pp.c0[j], pp.pw[j], pp.wc[j],
-                         xp.as<double>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], &run, s);
+                         xp.as<double>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], runp, st);
       else
         cg_panel<float>(g, hp_coeffs, ncoeffs, gamma, ridge, mask.as<uint8_t>(), didx.as<int64_t>(), n,
                         dred.as<double>(), k, tol, max_iters, pp.c0[j], pp.pw[j], pp.wc[j],
-                        xp.as<float>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], &run, s);
+                        xp.as<float>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], runp, st);
+    };
+    // A narrower remainder panel (e.g. k = 100 -> 32 + 32 + 32 + 4) is bound by row requests,
+    // not bytes: its CG runs on a side stream and host thread beside the main panels.  The
+    // panels share nothing but read-only inputs, so results are unchanged.
+    const int last = pp.np - 1;
+    const bool overlap = g_opt.cg_overlap.load() != 0 && pp.np > 1 && pp.pw[last] < pp.max_pw;
+    if (overlap) {
+      cudaStream_t ss = nullptr;
+      cudaEvent_t ready = nullptr, done = nullptr;
+      CSC_CUDA(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+      CSC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      CSC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      CSC_CUDA(cudaEventRecord(ready, s));
+      CSC_CUDA(cudaStreamWaitEvent(ss, ready, 0));
+      int64_t run_side = 0;
+      const int dev = g->device;
+      std::future<void> fut = SideWorker::get().submit([&, dev, ss] {
+        DeviceGuard sdg(dev);
+        panel(last, &run_side, ss);
+      });
+      std::exception_ptr err;
+      try {
+        for (int j = 0; j < last; ++j) panel(j, &run, s);
+      } catch (...) {
+        err = std::current_exception();
+      }
+      try {
+        fut.get();  // rethrows the side panel's failure
+      } catch (...) {
+        if (!err) err = std::current_exception();
+      }
+      cudaEventRecord(done, ss);
+      cudaStreamWaitEvent(s, done, 0);
+      cudaEventDestroy(ready);
+      cudaEventDestroy(done);
+      cudaStreamDestroy(ss);
+      if (err) std::rethrow_exception(err);
+      run = std::max(run, run_side);
+    } else {
+      for (int j = 0; j < pp.np; ++j) panel(j, &run, s);
     }
     if (N > 0) {
       const bool xdev = is_device_ptr(X_out, g->device);

@@ -75,6 +75,7 @@ struct Options {
   std::atomic<int64_t> l2_persist_pct{0}; // >0: keep the gathered panel in a persisting L2 window
   std::atomic<int64_t> persistent{1};     // 1: step grid = resident CTAs (grid-stride); 0: one CTA per row block
   std::atomic<int64_t> cg_compact{1};     // block CG: move still-active columns into narrower panels
+  std::atomic<int64_t> cg_overlap{1};     // block CG: a narrower remainder panel runs on a side stream
   std::atomic<int64_t> lean_mid{1};       // K2: 32-register mid-step kernel (64 warps/SM) for the hot case
   std::atomic<int64_t> fast_normalize{1}; // K3: vectorised single-panel row normalisation
 };

@@ -174,6 +174,7 @@ static std::atomic<int64_t>* option_slot(const char* key) {
   if (k == "panel_width") return &g_opt.panel_width;
   if (k == "recurrence") return &g_opt.recurrence;
   if (k == "cache_hints") return &g_opt.cache_hints;
+  if (k == "cg_overlap") return &g_opt.cg_overlap;
   if (k == "lean_mid") return &g_opt.lean_mid;
   if (k == "fast_normalize") return &g_opt.fast_normalize;
   if (k == "block_threads") return &g_opt.block_threads;

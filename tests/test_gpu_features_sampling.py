@@ -293,3 +293,23 @@ def test_fast_single_panel_normalisation_bit_identical(c1_golden, dtype):
             gi.num_nodes - 5, gi.num_nodes - 4, gi.num_nodes - 3], w
         rows, zero = O.build_features(low.coeffs, O.Csr(gi.num_nodes, gi.indptr, gi.indices, gi.weights, gi.degrees), X)
         assert relerr(out[1][0], rows) <= (1e-9 if dtype == "float64" else 1e-4), w
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_block_cg_remainder_panel_overlap_is_exact(c1_golden, dtype):
+    """k = 20 in 8-wide panels (8 + 8 + 4): the 4-wide remainder panel's CG runs on the side
+    stream / worker thread (cg_overlap=1) or in line (0) with bit-identical X, iteration counts
+    and residuals, both matching the reference."""
+    hp = P.matched_highpass(P.design_lowpass(float(c1_golden["lambda_k_hat"]), 50))
+    cfg = P.InterpolationConfig(highpass=hp)
+    samp = P.SamplingSet(indices=c1_golden["indices"], num_nodes=1000)
+    res = {}
+    for ov in (0, 1):
+        with options(panel_width=8, cg_overlap=ov):
+            res[ov] = P.interpolate_all(c1_op(dtype), cfg, samp, reduced_c1(c1_golden))
+    (X0, i0), (X1, i1) = res[0], res[1]
+    assert np.array_equal(X0, X1)
+    assert np.array_equal(i0.iterations, i1.iterations) and np.array_equal(i0.residuals, i1.residuals)
+    assert relerr(X1, c1_golden["soft"]) <= (1e-9 if dtype == "float64" else 1e-4)
+    if dtype == "float64":
+        assert np.array_equal(i1.iterations, c1_golden["solver_iterations"])
