@@ -514,11 +514,23 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
                         dred.as<double>(), k, tol, max_iters, pp.c0[j], pp.pw[j], pp.wc[j],
                         xp.as<float>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], runp, st);
     };
-    // A narrower remainder panel (e.g. k = 100 -> 32 + 32 + 32 + 4) is bound by row requests,
-    // not bytes: its CG runs on a side stream and host thread beside the main panels.  The
-    // panels share nothing but read-only inputs, so results are unchanged.
+    // The panels share nothing but read-only inputs, so running two at once leaves every
+    // result unchanged.
+    // Two ways to keep a second panel's CG running beside the first (option cg_overlap: 0 off,
+    // 1 auto, 2 always split):
+    //  * remainder: a narrower last panel (k = 100 -> 32 + 32 + 32 + 4) is bound by row
+    //    requests, not bytes; it runs beside the main panels (C3 CSC -2 %);
+    //  * split: panels of 512-B rows (one row per warp, little memory-level parallelism per
+    //    warp) whose gather source is <= 4x L2 alternate between the two streams (C4 k = 250:
+    //    CG 0.48 -> 0.35 s).  Splitting 128-B-row panels is slower (C3 +1 %, C5 +40 %: the
+    //    concurrent gather sources thrash L2 and DRAM).
     const int last = pp.np - 1;
-    const bool overlap = g_opt.cg_overlap.load() != 0 && pp.np > 1 && pp.pw[last] < pp.max_pw;
+    const int64_t ovmode = g_opt.cg_overlap.load();
+    const bool remainder = ovmode == 1 && pp.np > 1 && pp.pw[last] < pp.max_pw;
+    const bool split = pp.np > 1 && !remainder &&
+                       (ovmode == 2 || (ovmode == 1 && (size_t)pp.max_pw * cs == 512 &&
+                                        (double)N * pp.max_pw * cs <= 4.0 * device_props(g->device).l2_bytes));
+    const bool overlap = remainder || split;
     if (overlap) {
       cudaStream_t ss = nullptr;
       cudaEvent_t ready = nullptr, done = nullptr;
@@ -531,11 +543,19 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
       const int dev = g->device;
       std::future<void> fut = SideWorker::get().submit([&, dev, ss] {
         DeviceGuard sdg(dev);
-        panel(last, &run_side, ss);
+        if (split) {
+          for (int j = 1; j < pp.np; j += 2) panel(j, &run_side, ss);
+        } else {
+          panel(last, &run_side, ss);
+        }
       });
       std::exception_ptr err;
       try {
-        for (int j = 0; j < last; ++j) panel(j, &run, s);
+        if (split) {
+          for (int j = 0; j < pp.np; j += 2) panel(j, &run, s);
+        } else {
+          for (int j = 0; j < last; ++j) panel(j, &run, s);
+        }
       } catch (...) {
         err = std::current_exception();
       }
