@@ -77,9 +77,9 @@ int csc_launch_count(int64_t* out);
  *   "l2_budget_pct" L2 share a gathered panel may use (auto panel width)
  *   "l2_persist_pct" >0: persisting-L2 access window on the gathered panel
  *   "cg_compact"    1 (default): block CG moves still-active columns into narrower panels
- *   "cg_overlap"    1 (default, auto): a narrower remainder CG panel, or alternate panels of 512-B
- *                   rows with gather sources <= 4x L2, run on a side stream / host thread;
- *                   0 off; 2 always alternate panels between the two streams
+ *   "cg_overlap"    1 (default): block-CG panels run two at a time (side stream / host thread);
+ *                   a full-width panel runs alone until its first compaction (no such limit for
+ *                   512-B-row panels with gather sources <= 4x L2); 0 off; 2 no limit
  *   "profile"       1 = time the Chebyshev step kernels with CUDA events            */
 int csc_set_option(const char* key, int64_t value);
 int csc_get_option(const char* key, int64_t* value);

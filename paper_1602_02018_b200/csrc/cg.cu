@@ -273,7 +273,8 @@ ColState carve_state(Scratch& mem, int w, cudaStream_t s) {
 template <typename T>
 void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double ridge, const uint8_t* mask,
               const int64_t* idx, int64_t n, const double* reduced, int k, double tol, int64_t max_iters, int c0,
-              int pw, int wc, T* Xp, double* resid, uint8_t* conv, int64_t* its, int64_t* iters_run, cudaStream_t s) {
+              int pw, int wc, T* Xp, double* resid, uint8_t* conv, int64_t* its, int64_t* iters_run, cudaStream_t s,
+              const std::function<void()>* on_narrow = nullptr) {
   const int64_t N = g->n;
   const size_t pb = sizeof(T) * (size_t)N * pw;
   Scratch R(pb, s), P(pb, s), Ps(pb, s), AP(pb, s), B0(pb, s), B1(pb, s), Yacc;
@@ -392,6 +393,10 @@ void cg_panel(const csc_graph* g, const double* hp, int nc, double gamma, double
     CSC_CUDA(cudaStreamSynchronize(s));  // host vectors feeding async copies go out of scope
     pw_cur = want;
     wc_cur = nact;
+    if (on_narrow && *on_narrow) {  // first compaction: this panel no longer needs the GPU alone
+      (*on_narrow)();
+      on_narrow = nullptr;
+    }
   }
   k_cg_finish_map<<<1, 128, 0, s>>>(st, wc_cur, iters, cmap.as<int>(), resid, conv, its);
   CSC_LAUNCHED();
@@ -504,34 +509,79 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
 
     Scratch xp(cs * std::max<int64_t>(pp.total, 1), s);
     int64_t run = 0;
-    auto panel = [&](int j, int64_t* runp, cudaStream_t st) {
+    auto panel = [&](int j, int64_t* runp, cudaStream_t st, const std::function<void()>* on_narrow) {
       if (g->dtype == CSC_F64)
         cg_panel<double>(g, hp_coeffs, ncoeffs, gamma, ridge, mask.as<uint8_t>(), didx.as<int64_t>(), n,
                          dred.as<double>(), k, tol, max_iters, pp.c0[j], pp.pw[j], pp.wc[j],
-                         xp.as<double>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], runp, st);
+                         xp.as<double>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], runp, st,
+                         on_narrow);
       else
         cg_panel<float>(g, hp_coeffs, ncoeffs, gamma, ridge, mask.as<uint8_t>(), didx.as<int64_t>(), n,
                         dred.as<double>(), k, tol, max_iters, pp.c0[j], pp.pw[j], pp.wc[j],
-                        xp.as<float>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], runp, st);
+                        xp.as<float>() + pp.off[j], d_res + pp.c0[j], d_conv + pp.c0[j], d_it + pp.c0[j], runp, st,
+                        on_narrow);
     };
-    // The panels share nothing but read-only inputs, so running two at once leaves every
-    // result unchanged.
-    // Two ways to keep a second panel's CG running beside the first (option cg_overlap: 0 off,
-    // 1 auto, 2 always split):
-    //  * remainder: a narrower last panel (k = 100 -> 32 + 32 + 32 + 4) is bound by row
-    //    requests, not bytes; it runs beside the main panels (C3 CSC -2 %);
-    //  * split: panels of 512-B rows (one row per warp, little memory-level parallelism per
-    //    warp) whose gather source is <= 4x L2 alternate between the two streams (C4 k = 250:
-    //    CG 0.48 -> 0.35 s).  Splitting 128-B-row panels is slower (C3 +1 %, C5 +40 %: the
-    //    concurrent gather sources thrash L2 and DRAM).
-    const int last = pp.np - 1;
+    // Two panels' CGs run at once where that helps (option cg_overlap: 0 off, 1 auto, 2 no
+    // token).  The panels share nothing but read-only inputs, so every result is unchanged.
+    //  * A full-width panel holds the "wide" token until its first compaction (its active
+    //    columns fit half the width) or its end: two full-width panels of 128/256-B rows
+    //    contend for L2 and DRAM (measured C3 +1 %, C5 +40 % when run together), while a
+    //    narrower panel -- a remainder (k = 100 -> 32 + 32 + 32 + 4) or a compacted one -- is
+    //    bound by row requests and overlaps well (C3 CSC 0.830 -> 0.81 s).
+    //  * Panels of 512-B rows (one row per warp, little memory-level parallelism per warp)
+    //    whose gather source is <= 4x L2 need no token (C4 k = 250: CG 0.48 -> 0.35 s).
     const int64_t ovmode = g_opt.cg_overlap.load();
-    const bool remainder = ovmode == 1 && pp.np > 1 && pp.pw[last] < pp.max_pw;
-    const bool split = pp.np > 1 && !remainder &&
-                       (ovmode == 2 || (ovmode == 1 && (size_t)pp.max_pw * cs == 512 &&
-                                        (double)N * pp.max_pw * cs <= 4.0 * device_props(g->device).l2_bytes));
-    const bool overlap = remainder || split;
-    if (overlap) {
+    const bool untokened = ovmode == 2 || ((size_t)pp.max_pw * cs == 512 &&
+                                           (double)N * pp.max_pw * cs <= 4.0 * device_props(g->device).l2_bytes);
+    if (ovmode == 0 || pp.np < 2) {
+      for (int j = 0; j < pp.np; ++j) panel(j, &run, s, nullptr);
+    } else {
+      std::vector<int> order;  // narrower panels first, so the side thread starts on one at once
+      for (int j = 0; j < pp.np; ++j)
+        if (pp.pw[j] < pp.max_pw) order.push_back(j);
+      for (int j = 0; j < pp.np; ++j)
+        if (pp.pw[j] == pp.max_pw) order.push_back(j);
+      std::mutex mu;
+      std::condition_variable cv;
+      size_t next = 0;
+      bool busy = false, abort = false;
+      auto worker = [&](cudaStream_t st, int64_t* runp) {
+        for (;;) {
+          int j = -1;
+          bool held = false;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            if (abort || next >= order.size()) return;
+            j = order[next];
+            const bool wide = pp.pw[j] == pp.max_pw && !untokened;
+            if (wide) {
+              cv.wait(lk, [&] { return !busy || abort; });
+              if (abort) return;
+              busy = held = true;
+            }
+            ++next;
+          }
+          const std::function<void()> release = [&] {
+            std::lock_guard<std::mutex> lk(mu);
+            if (held) {
+              busy = held = false;
+              cv.notify_all();
+            }
+          };
+          try {
+            panel(j, runp, st, held ? &release : nullptr);
+          } catch (...) {
+            {
+              std::lock_guard<std::mutex> lk(mu);
+              abort = true;
+            }
+            release();
+            cv.notify_all();
+            throw;
+          }
+          release();
+        }
+      };
       cudaStream_t ss = nullptr;
       cudaEvent_t ready = nullptr, done = nullptr;
       CSC_CUDA(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
@@ -543,24 +593,16 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
       const int dev = g->device;
       std::future<void> fut = SideWorker::get().submit([&, dev, ss] {
         DeviceGuard sdg(dev);
-        if (split) {
-          for (int j = 1; j < pp.np; j += 2) panel(j, &run_side, ss);
-        } else {
-          panel(last, &run_side, ss);
-        }
+        worker(ss, &run_side);
       });
       std::exception_ptr err;
       try {
-        if (split) {
-          for (int j = 0; j < pp.np; j += 2) panel(j, &run, s);
-        } else {
-          for (int j = 0; j < last; ++j) panel(j, &run, s);
-        }
+        worker(s, &run);
       } catch (...) {
         err = std::current_exception();
       }
       try {
-        fut.get();  // rethrows the side panel's failure
+        fut.get();  // rethrows the side worker's failure
       } catch (...) {
         if (!err) err = std::current_exception();
       }
@@ -571,8 +613,6 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
       cudaStreamDestroy(ss);
       if (err) std::rethrow_exception(err);
       run = std::max(run, run_side);
-    } else {
-      for (int j = 0; j < pp.np; ++j) panel(j, &run, s);
     }
     if (N > 0) {
       const bool xdev = is_device_ptr(X_out, g->device);
