@@ -80,21 +80,35 @@ __device__ inline double fast_value(uint64_t u) {
   }
 }
 
-constexpr int kChunk = 64;  // raws per thread
 
 template <Dist D>
 __global__ void k_pcg_raw(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, int64_t m,
                           uint64_t* __restrict__ raw, uint8_t* __restrict__ special) {
+  // Thread t of T produces raws t, t + T, t + 2T, ...: consecutive threads write consecutive
+  // positions (coalesced stores).  Raw p is the output of the state after p + 1 LCG steps;
+  // moving T positions ahead is the affine map st -> A st + C of T steps.
   const u128 inc = make128(i_hi, i_lo);
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c * kChunk < m; c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i0 = c * kChunk;
-    u128 st = pcg_advance(make128(s_hi, s_lo), inc, (uint64_t)i0);
-    const int64_t i1 = min(m, i0 + kChunk);
-    for (int64_t i = i0; i < i1; ++i) {
-      const uint64_t u = pcg_next(st, inc);
-      raw[i] = u;
-      special[i] = is_special<D>(u) ? 1 : 0;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  if (t >= m) return;
+  u128 A = 1, C = 0, cur_mult = pcg_mult(), cur_plus = inc;
+  for (uint64_t delta = (uint64_t)T; delta; delta >>= 1) {
+    if (delta & 1) {
+      A *= cur_mult;
+      C = C * cur_mult + cur_plus;
     }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+  }
+  u128 st = pcg_advance(make128(s_hi, s_lo), inc, (uint64_t)t + 1);
+  for (int64_t i = t; i < m; i += T) {
+    const uint64_t hi = (uint64_t)(st >> 64), lo = (uint64_t)st;  // numpy's XSL-RR output of st
+    const uint64_t x = hi ^ lo;
+    const unsigned r = (unsigned)(hi >> 58);
+    const uint64_t u = (x >> r) | (x << ((64u - r) & 63u));
+    raw[i] = u;
+    special[i] = is_special<D>(u) ? 1 : 0;
+    st = A * st + C;
   }
 }
 
@@ -388,8 +402,10 @@ int64_t numpy_draws(const Tables& t, u128 s0, u128 inc, int64_t count, double di
   for (int attempt = 0; attempt < 4; ++attempt, m = m * 2) {
     // 1. raws + special flags; compact the special positions (stable)
     Scratch raw(sizeof(uint64_t) * m, s, mp), special(m, s, mp);
-    const int64_t chunks = (m + kChunk - 1) / kChunk;
-    k_pcg_raw<D><<<(int)std::min<int64_t>((chunks + 255) / 256, 65535), 256, 0, s>>>(
+    int dev_now = 0;
+    CSC_CUDA(cudaGetDevice(&dev_now));
+    const int64_t pblocks = std::min<int64_t>((m + 255) / 256, (int64_t)device_props(dev_now).sms * 8);
+    k_pcg_raw<D><<<(int)std::max<int64_t>(pblocks, 1), 256, 0, s>>>(
         s_hi, s_lo, inc_hi, inc_lo, m, raw.as<uint64_t>(), special.as<uint8_t>());
     CSC_LAUNCHED();
     Scratch pos(sizeof(int64_t) * m, s, mp), nsel(2 * sizeof(int64_t), s, mp);
