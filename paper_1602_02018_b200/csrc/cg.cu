@@ -532,9 +532,8 @@ extern "C" int csc_block_cg(const csc_graph* g, const double* hp_coeffs, int nco
     //    whose gather source is <= 4x L2 need no token (C4 k = 250: CG 0.48 -> 0.35 s).
     //  * Gather sources above 4x L2 (C5: 2 GB per 32-wide panel) run one panel at a time.
     const int64_t ovmode = g_opt.cg_overlap.load();
-    const bool untokened = ovmode == 2 || ((size_t)pp.max_pw * cs == 512 &&
-                                           (double)N * pp.max_pw * cs <= 4.0 * device_props(g->device).l2_bytes);
     const bool small_source = (double)N * pp.max_pw * cs <= 4.0 * device_props(g->device).l2_bytes;
+    const bool untokened = ovmode == 2 || ((size_t)pp.max_pw * cs == 512 && small_source);
     if (ovmode == 0 || pp.np < 2 || (ovmode == 1 && !small_source)) {  // C5's 2 GB panels: +6 % overlapped
       for (int j = 0; j < pp.np; ++j) panel(j, &run, s, nullptr);
     } else {
