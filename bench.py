@@ -115,6 +115,9 @@ class ClockSampler:
     def __exit__(self, *a):
         if self.proc:
             time.sleep(0.25)
+            t_end = time.time() + 5.0  # a short timed region may end before nvidia-smi's first sample
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.05)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
