@@ -97,6 +97,8 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines: list[str] = []
+        self.stamps: list[float] = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -111,11 +113,19 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self.stamps.append(time.perf_counter())
+
+    def mark(self, start: bool):
+        """Bracket the timed region (samples are taken every 100 ms from __enter__ on)."""
+        if start:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
 
     def __exit__(self, *a):
         if self.proc:
             time.sleep(0.25)
-            t_end = time.time() + 5.0  # a short timed region may end before nvidia-smi's first sample
+            t_end = time.time() + 5.0  # at least one sample, even if the region was very short
             while not self.lines and time.time() < t_end and self.proc.poll() is None:
                 time.sleep(0.05)
             self.proc.terminate()
@@ -123,7 +133,14 @@ class ClockSampler:
 
     def summary(self):
         rows = []
-        for ln in self.lines:
+        lines = list(zip(self.stamps, self.lines))
+        if self.t0 is not None and self.t1 is not None and lines:
+            inside = [ln for t, ln in lines if self.t0 <= t <= self.t1 + 0.1]
+            # a region shorter than the 100 ms sampling period: the sample nearest to it
+            lines = inside or [min(lines, key=lambda x: abs(x[0] - 0.5 * (self.t0 + self.t1)))[1]]
+        else:
+            lines = [ln for _, ln in lines]
+        for ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) == 7:
                 try:
@@ -326,22 +343,26 @@ def run_ours(args, cfg):
             sharded_features(backend, filt, X, grp)
 
 
-    for _ in range(args.warmup):
-        step_device()
-    barrier()
-    torch.cuda.synchronize()
-    gc.collect()
-    gc.disable()  # no collector pauses inside the timed regions (value and e2e); re-enabled below
-    _lib.set_option("profile", 1)
-    _lib.profile_reset()
-    l0 = _lib.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the clock sampler runs from the warm-up on (nvidia-smi needs ~0.2 s for its first sample);
+    # only samples inside the marked timed region are reported
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            step_device()
+        barrier()
+        torch.cuda.synchronize()
+        gc.collect()
+        gc.disable()  # no collector pauses inside the timed regions (value and e2e); re-enabled below
+        _lib.set_option("profile", 1)
+        _lib.profile_reset()
+        l0 = _lib.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks.mark(True)
         e0.record(stream)
         for _ in range(args.steps):
             step_device()
         e1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark(False)
     barrier()
     launches = _lib.launch_count() - l0
     step_ms, step_launches, step_bytes = _lib.profile_read()
