@@ -314,3 +314,25 @@ def test_block_cg_remainder_panel_overlap_is_exact(c1_golden, dtype):
     assert relerr(X1, c1_golden["soft"]) <= (1e-9 if dtype == "float64" else 1e-4)
     if dtype == "float64":
         assert np.array_equal(i1.iterations, c1_golden["solver_iterations"])
+
+
+def test_block_cg_two_wide_panels_split_streams_exact(c1_golden):
+    """fp32, k = 200 on C1: two 128-wide panels of 512-B rows with a small gather source, the
+    case the CG scheduler runs on two streams without the full-width token; results must be
+    bit-identical to the in-line run and within the fp32 bar of the oracle."""
+    hp = P.matched_highpass(P.design_lowpass(float(c1_golden["lambda_k_hat"]), 50))
+    cfg = P.InterpolationConfig(highpass=hp)
+    samp = P.SamplingSet(indices=c1_golden["indices"], num_nodes=1000)
+    n, k = c1_golden["indices"].size, 200
+    reduced = np.zeros((n, k))
+    reduced[np.arange(n), np.random.default_rng(4).integers(0, k, n)] = 1.0
+    res = {}
+    for ov in (0, 1):
+        with options(cg_overlap=ov):
+            res[ov] = P.interpolate_all(c1_op("float32"), cfg, samp, reduced)
+    (X0, i0), (X1, i1) = res[0], res[1]
+    assert np.array_equal(X0, X1) and np.array_equal(i0.iterations, i1.iterations)
+    g, _ = c1_graph()
+    X, its, _, _ = O.interpolate_all(oracle_csr(g), hp.coeffs, cfg.gamma, cfg.ridge, samp.indices, reduced,
+                                     cfg.solver_tol, cfg.solver_max_iters)
+    assert relerr(X1, X) <= 1e-4
