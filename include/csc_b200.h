@@ -162,7 +162,8 @@ int csc_eigencount(const csc_graph* g, const double* coeffs, int ncoeffs, const 
                    int ncols, int io_dtype, double* count, void* stream);
 
 /* F = rownormalize(h(L) R).  Rows whose norm is <= 1e-300 are left zero and
- * flagged in zero_flags[N] (uint8, may be NULL); *num_zero receives their count.
+ * flagged in zero_flags[N] (uint8, may be NULL); *num_zero receives their count
+ * (num_zero NULL: no host synchronisation when F and zero_flags are device buffers).
  * Replaces build_features (features.py:70-93, norm rule at :80-87). */
 int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, const void* R, int64_t ldr,
                        int ncols, int io_dtype, void* F, int64_t ldf, uint8_t* zero_flags, int64_t* num_zero,

@@ -1449,24 +1449,11 @@ int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, co
       run_filter_all<double>(g, coeffs, ncoeffs, in, yp.as<double>(), EPI_ROWSQ, rowsq.as<double>(), n, s);
     else
       run_filter_all<float>(g, coeffs, ncoeffs, in, yp.as<float>(), EPI_ROWSQ, rowsq.as<double>(), n, s);
-    // panel tables for the normaliser
-    std::vector<int> meta(3 * pp.np);
-    for (int j = 0; j < pp.np; ++j) {
-      meta[j] = pp.pw[j];
-      meta[pp.np + j] = pp.wc[j];
-      meta[2 * pp.np + j] = pp.c0[j];
-    }
-    Scratch dmeta(sizeof(int) * meta.size(), s), doff(sizeof(int64_t) * pp.np, s);
-    CSC_CUDA(cudaMemcpyAsync(dmeta.get(), meta.data(), sizeof(int) * meta.size(), cudaMemcpyHostToDevice, s));
-    CSC_CUDA(cudaMemcpyAsync(doff.get(), pp.off.data(), sizeof(int64_t) * pp.np, cudaMemcpyHostToDevice, s));
     StagedOut fo;
     stage_out(F, ldf, n, ncols, io_dtype, g->device, s, fo);
     DeviceOut zo(zero_flags, (size_t)n, g->device, s);
     Scratch nz(sizeof(unsigned long long), s);
     CSC_CUDA(cudaMemsetAsync(nz.get(), 0, sizeof(unsigned long long), s));
-    const int* pw = dmeta.as<int>();
-    const int* wc = pw + pp.np;
-    const int* c0 = pw + 2 * pp.np;
     const int grid = (int)std::min<int64_t>((n + 7) / 8, (int64_t)device_props(g->device).sms * 16);
     bool done = false;
     if (g_opt.fast_normalize.load()) {
@@ -1482,6 +1469,24 @@ int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, co
       else
         done = launch_normalize_1p<float, float>(pp, yp.as<float>(), rowsq.as<double>(), n, (float*)fo.p, fo.ld,
                                                  zo.as<uint8_t>(), nz.as<unsigned long long>(), g->device, s);
+    }
+    // panel tables for the general normaliser (pageable copies: only when it runs)
+    Scratch dmeta, doff;
+    const int *pw = nullptr, *wc = nullptr, *c0 = nullptr;
+    if (!done) {
+      std::vector<int> meta(3 * pp.np);
+      for (int j = 0; j < pp.np; ++j) {
+        meta[j] = pp.pw[j];
+        meta[pp.np + j] = pp.wc[j];
+        meta[2 * pp.np + j] = pp.c0[j];
+      }
+      dmeta.alloc(sizeof(int) * meta.size(), s);
+      doff.alloc(sizeof(int64_t) * pp.np, s);
+      CSC_CUDA(cudaMemcpyAsync(dmeta.get(), meta.data(), sizeof(int) * meta.size(), cudaMemcpyHostToDevice, s));
+      CSC_CUDA(cudaMemcpyAsync(doff.get(), pp.off.data(), sizeof(int64_t) * pp.np, cudaMemcpyHostToDevice, s));
+      pw = dmeta.as<int>();
+      wc = pw + pp.np;
+      c0 = pw + 2 * pp.np;
     }
     if (done) {
     } else if (g->dtype == CSC_F64 && io_dtype == CSC_F64)
@@ -1503,10 +1508,13 @@ int csc_build_features(const csc_graph* g, const double* coeffs, int ncoeffs, co
     if (!done) CSC_LAUNCHED();
     finish_out(fo, n, ncols, io_dtype, s);
     zo.finish();
-    unsigned long long hz = 0;
-    CSC_CUDA(cudaMemcpyAsync(&hz, nz.get(), sizeof(hz), cudaMemcpyDeviceToHost, s));
-    CSC_CUDA(cudaStreamSynchronize(s));
-    if (num_zero) *num_zero = (int64_t)hz;
+    // num_zero NULL with device outputs: no host readback, the call stays asynchronous
+    if (num_zero || fo.host || zo.on_host()) {
+      unsigned long long hz = 0;
+      CSC_CUDA(cudaMemcpyAsync(&hz, nz.get(), sizeof(hz), cudaMemcpyDeviceToHost, s));
+      CSC_CUDA(cudaStreamSynchronize(s));
+      if (num_zero) *num_zero = (int64_t)hz;
+    }
   });
 }
 

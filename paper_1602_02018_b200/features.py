@@ -83,11 +83,13 @@ def _provenance(filt: PolyFilter, signals: RandomSignals) -> dict:
     }
 
 
-def features_into(op, filt: PolyFilter, matrix, out) -> np.ndarray:
+def features_into(op, filt: PolyFilter, matrix, out, *, zero_rows: bool = True) -> np.ndarray | None:
     """Filter + row-normalise ``matrix`` into ``out``; returns the zero-row indices.
 
     ``matrix``/``out`` are both host arrays (fp64) or both CUDA tensors of the
-    same dtype.  Zero-row flags stay on the device for device outputs.
+    same dtype.  Zero-row flags stay on the device for device outputs.  With
+    ``zero_rows=False`` and device buffers the call does not synchronise with the
+    host (the zero rows are still left zero) and returns None.
     """
     blk = as_block(matrix, op.num_nodes, "signals")
     ob = as_block(out, op.num_nodes, "features")
@@ -96,6 +98,12 @@ def features_into(op, filt: PolyFilter, matrix, out) -> np.ndarray:
     if blk.code != ob.code:
         raise ValueError("signals and features must share a dtype")
     c = coeff_array(filt)
+    if not zero_rows and ob.on_device:
+        _lib.call(
+            "csc_build_features", op.handle, _lib.ptr(c), int(c.size), blk.ptr, blk.ld, blk.ncols, blk.code, ob.ptr,
+            ob.ld, None, None, _lib.current_stream(op.device),
+        )
+        return None
     if ob.on_device:
         import torch
 

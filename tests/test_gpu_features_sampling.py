@@ -336,3 +336,18 @@ def test_block_cg_two_wide_panels_split_streams_exact(c1_golden):
     X, its, _, _ = O.interpolate_all(oracle_csr(g), hp.coeffs, cfg.gamma, cfg.ridge, samp.indices, reduced,
                                      cfg.solver_tol, cfg.solver_max_iters)
     assert relerr(X1, X) <= 1e-4
+
+
+def test_features_async_device_call_matches(c1_golden):
+    """features_into(..., zero_rows=False) on device buffers (no host synchronisation) writes the
+    same features as the synchronous call."""
+    import torch
+
+    op = c1_op("float32")
+    X = torch.tensor(np.random.default_rng(2).standard_normal((1000, 28)), device="cuda", dtype=torch.float32)
+    low = P.design_lowpass(0.4, 30)
+    F0, F1 = torch.empty_like(X), torch.empty_like(X)
+    z = P.features.features_into(op, low, X, F0)
+    assert P.features.features_into(op, low, X, F1, zero_rows=False) is None
+    torch.cuda.synchronize()
+    assert z.size == 0 and torch.equal(F0, F1)
