@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--async-steps", action="store_true", help="features_into(..., zero_rows=False)")
+    ap.add_argument("--csc", action="store_true", help="profile one warm run_csc instead of feature steps")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -40,9 +41,17 @@ def main():
     for _ in range(3):
         features_into(op, filt, X, F)
     torch.cuda.synchronize()
+    if args.csc:
+        prm = P.CscParams(k=cfg["k"], d=d, seed=0)
+        P.run_csc(op, prm)
+        torch.cuda.synchronize()
+        args.steps = 1
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(args.steps):
-            features_into(op, filt, X, F, zero_rows=not args.async_steps)
+            if args.csc:
+                P.run_csc(op, prm)
+            else:
+                features_into(op, filt, X, F, zero_rows=not args.async_steps)
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
     evs.sort(key=lambda e: e.time_range.start)
