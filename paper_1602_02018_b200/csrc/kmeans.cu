@@ -89,6 +89,94 @@ __device__ double pw_sum(const F& v, int64_t off, int64_t n) {
   return ret;
 }
 
+// numpy's pairwise sum over n elements evaluated by a whole CTA: the leaves of the
+// recursion (blocks of <= 128 elements, each summed with pw_leaf's 8 accumulators) are
+// independent, so threads sum them in parallel; one thread then combines the leaf sums in
+// the recursion's order (a postfix program built once per kernel).  Bit-identical to pw_sum.
+constexpr int kMaxLeaves = 512;
+struct PwPlan {
+  int nleaf, nprog;  // nleaf < 0: too many leaves, use pw_sum
+  int off[kMaxLeaves];
+  int len[kMaxLeaves];
+  short prog[2 * kMaxLeaves];  // >= 0: push leaf sum, -1: add the top two
+};
+
+__device__ void pw_plan_build(PwPlan& pl, int64_t n) {  // one thread
+  pl.nleaf = pl.nprog = 0;
+  if (n <= 128) {
+    pl.off[0] = 0;
+    pl.len[0] = (int)n;
+    pl.prog[0] = 0;
+    pl.nleaf = pl.nprog = 1;
+    return;
+  }
+  int64_t so[48], sn[48];
+  int ss[48];
+  int sp = 0;
+  so[0] = 0;
+  sn[0] = n;
+  ss[0] = 0;
+  while (sp >= 0) {
+    int64_t n2 = sn[sp] / 2;
+    n2 -= n2 % 8;
+    if (ss[sp] == 0 || ss[sp] == 1) {  // 0: left half, 1: right half
+      const int64_t o = ss[sp] == 0 ? so[sp] : so[sp] + n2;
+      const int64_t m = ss[sp] == 0 ? n2 : sn[sp] - n2;
+      ++ss[sp];
+      if (m > 128) {
+        ++sp;
+        so[sp] = o;
+        sn[sp] = m;
+        ss[sp] = 0;
+        continue;
+      }
+      if (pl.nleaf >= kMaxLeaves) {
+        pl.nleaf = -1;
+        return;
+      }
+      pl.off[pl.nleaf] = (int)o;
+      pl.len[pl.nleaf] = (int)m;
+      pl.prog[pl.nprog++] = (short)pl.nleaf++;
+      continue;
+    }
+    pl.prog[pl.nprog++] = -1;  // both halves done: left + right
+    --sp;
+  }
+}
+
+// Called by every thread of the CTA; returns the sum to all of them.
+template <class F>
+__device__ double pw_sum_block(const F& v, int64_t n, const PwPlan& pl, double* leafval) {
+  __shared__ double s_res;
+  if (pl.nleaf < 0) {
+    if (threadIdx.x == 0) s_res = pw_sum(v, 0, n);
+    __syncthreads();
+    const double r = s_res;
+    __syncthreads();
+    return r;
+  }
+  for (int l = threadIdx.x; l < pl.nleaf; l += blockDim.x) leafval[l] = pw_leaf(v, pl.off[l], pl.len[l]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double st[64];
+    int sp = 0;
+    for (int t = 0; t < pl.nprog; ++t) {
+      const int op = pl.prog[t];
+      if (op >= 0) {
+        st[sp++] = leafval[op];
+      } else {
+        const double b = st[--sp];
+        st[sp - 1] = __dadd_rn(st[sp - 1], b);
+      }
+    }
+    s_res = st[0];
+  }
+  __syncthreads();
+  const double r = s_res;
+  __syncthreads();  // s_res / leafval reused by the next call
+  return r;
+}
+
 // (x * x).sum() of one row
 __device__ double sq_row(const double* x, int d) {
   return pw_sum([x](int64_t t) { return __dmul_rn(x[t], x[t]); }, 0, d);
@@ -153,7 +241,11 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
   __shared__ int64_t s_pick;
   __shared__ double s_inertia;
   __shared__ int s_rep;
+  __shared__ PwPlan s_plan;  // numpy's pairwise-sum tree over n points
+  __shared__ double s_leaf[kMaxLeaves];
   int status = 0;
+  if (tid == 0) pw_plan_build(s_plan, n);
+  __syncthreads();
 
   if (first) {
     // ---- k-means++ seeding (kmeans.py:52-61)
@@ -168,8 +260,9 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
     for (int64_t i = tid; i < n; i += kThreads) near[i] = sqdiff_col(P + i * d, C, k, 0, d);
     __syncthreads();
     for (int j = 1; j < k; ++j) {
+      const double total_all = pw_sum_block([near](int64_t i) { return near[i]; }, n, s_plan, s_leaf);
       if (tid == 0) {
-        const double total = pw_sum([near](int64_t i) { return near[i]; }, 0, n);
+        const double total = total_all;
         s_pick = (total > 0.0 && total < INFINITY) ? 0 : -1;
         s_inertia = total;
       }
@@ -272,8 +365,9 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
         __syncwarp();  // p is overwritten by the next point
       }
       __syncthreads();
+      const double inert_all = pw_sum_block([near](int64_t i) { return near[i]; }, n, s_plan, s_leaf);
       if (tid == 0) {
-        s_inertia = pw_sum([near](int64_t i) { return near[i]; }, 0, n);
+        s_inertia = inert_all;
         int acc = 0;
         for (int j = 0; j < k; ++j) {
           offs[j] = acc;
