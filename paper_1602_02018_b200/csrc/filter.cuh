@@ -38,6 +38,11 @@
 //   Clenshaw  b_l = c_l X - 2 Wn b_{l+1} - b_{l+2};  Y = c_0 X - Wn b_1 - b_2
 //             streams per step: gather b_{l+1}, read b_{l+2}, read X, write b_l     (4)
 // Both evaluate the same polynomial sum_l c_l T_l(L - I) X with p SpMM passes.
+//
+// Two step kernels: k_cheb_step (every case: weights, epilogues, forward mode, peer
+// stores) and k_cheb_mid, the mid step alone with only that case's state (32 or 40
+// registers, more warps or more gathers in flight), used for 16-512-B panel rows whose
+// gather source is <= 4x L2 (unit weights, or any weights in fp32); bit-identical results.
 #pragma once
 
 #include "internal.cuh"
