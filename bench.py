@@ -506,7 +506,13 @@ def main():
         for kv in args.option:
             key, val = kv.split("=")
             _lib.set_option(key, int(val))
-    run_ours(args, cfg)
+    try:
+        run_ours(args, cfg)
+    finally:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()  # local teardown; ranks may arrive at different times
 
 
 if __name__ == "__main__":
