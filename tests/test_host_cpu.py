@@ -271,3 +271,23 @@ def test_feature_dump_format_matches_reference():
         back = load_features(q)
     assert np.array_equal(back.rows, gold["rows"]) and back.zero_rows.tolist() == [2]
     assert back.normalized is True and back.provenance == prov
+
+
+def test_bench_reference_arm_contract_on_cpu():
+    """bench.py --impl reference (the reference algorithm on the host cores) prints one JSON line
+    with the contract's keys; C1 keeps it to a second."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "dtype", "config", "e2e", "cpu_baseline"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] in ("port", "reference")
