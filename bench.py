@@ -355,7 +355,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         gc.collect()
         gc.disable()  # no collector pauses inside the timed regions (value and e2e); re-enabled below
-        _lib.set_option("profile", 1)
+        _lib.set_option("profile", 2)  # one event pair per filter (per-launch events cost ~2 % of a step)
         _lib.profile_reset()
         l0 = _lib.launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -441,6 +441,8 @@ def run_ours(args, cfg):
         "kernel": "fused Chebyshev step SpMM: k_cheb_mid (mid steps) + k_cheb_step (first / last steps)",
         "peak_source": peak_src,
         "kernel_ms_per_launch": step_ms / max(step_launches, 1), "launches_timed": step_launches,
+        "kernel_timing": "CUDA events around each filter's back-to-back step launches on the launch stream "
+                         "(profile mode 2), divided by the launches",
         "algorithmic_bytes_per_launch": alg_per_step_set * args.steps / max(step_launches, 1),
         "algorithmic_unit": "SURVEY.md 8(d) B_step(d) = B_csr + 5 N d s per step launch (B_first on the first); "
                             "one launch per step when the block is one panel",

@@ -80,7 +80,8 @@ int csc_launch_count(int64_t* out);
  *   "cg_overlap"    1 (default): block-CG panels run two at a time (side stream / host thread);
  *                   a full-width panel runs alone until its first compaction (no such limit for
  *                   512-B-row panels with gather sources <= 4x L2); 0 off; 2 no limit
- *   "profile"       1 = time the Chebyshev step kernels with CUDA events            */
+ *   "profile"       1 = time every Chebyshev step launch with CUDA events; 2 = one event
+ *                   pair per filter (its step launches run back to back; less intrusive) */
 int csc_set_option(const char* key, int64_t value);
 int csc_get_option(const char* key, int64_t* value);
 /* Profile counters of the Chebyshev step kernels since the last reset:

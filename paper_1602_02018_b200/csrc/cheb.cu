@@ -602,7 +602,7 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   if (a.n > 0 && (uint64_t)a.n * (uint64_t)lpr >= (1ull << 32))
     fail(CSC_ERR_INVALID, "panel too large for 32-bit vector offsets (rows x lanes >= 2^32)");
   const int threads = (int)g_opt.block_threads.load();
-  const bool prof = g_opt.profile.load() != 0 && a.G != nullptr;
+  const bool prof = g_opt.profile.load() == 1 && a.G != nullptr;  // 2: per filter span (filter_panel)
   cudaEvent_t e0 = nullptr;
   if (prof) profile_begin(s, &e0);
   int grid = 0;
@@ -669,6 +669,13 @@ int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, const 
     a.hz = hz;
     return a;
   };
+  // profile mode 2: one event pair around the whole filter (the step launches back to back),
+  // counted as its SpMM launches -- per-launch events cost ~2 % of a step at C3
+  const bool span = g_opt.profile.load() == 2;
+  cudaEvent_t span_e0 = nullptr;
+  double span_bytes = 0.0;
+  int64_t span_launches = 0;
+  if (span) profile_begin(s, &span_e0);
   auto run = [&](StepArgs a, int e) {
     if (e != EPI_NONE) {
       a.part = ex.part;
@@ -680,7 +687,13 @@ int filter_panel(const csc_graph* g, const double* c, int nc, const T* X, const 
       a.ridge = ex.ridge;
       a.E = ex.ap;
     }
-    return launch_step<T>(g, a, pw, e, s);
+    if (span && a.G != nullptr) {
+      span_bytes += step_bytes(g, a, e);
+      ++span_launches;
+    }
+    const int grid = launch_step<T>(g, a, pw, e, s);
+    if (span && a.last) profile_end(s, span_e0, span_bytes, span_launches);  // the filter's final step
+    return grid;
   };
 
   if (p == 0) {  // order 0: Y = c_0 X (filters.py:147)

@@ -89,7 +89,7 @@ struct Profile {
 // Non-blocking kernel profiling: a launch is bracketed by two pooled events
 // and its algorithmic bytes are recorded; csc_profile_read resolves them.
 void profile_begin(cudaStream_t s, cudaEvent_t* e0);
-void profile_end(cudaStream_t s, cudaEvent_t e0, double bytes);
+void profile_end(cudaStream_t s, cudaEvent_t e0, double bytes, int64_t launches = 1);
 
 // ---- device context -------------------------------------------------------
 struct DeviceGuard {

@@ -18,6 +18,7 @@ static Profile g_prof;
 struct PendingLaunch {
   cudaEvent_t e0, e1;
   double bytes;
+  int64_t launches;
 };
 static std::vector<PendingLaunch> g_pending;
 static std::vector<cudaEvent_t> g_event_pool;
@@ -40,11 +41,11 @@ void profile_begin(cudaStream_t s, cudaEvent_t* e0) {
   CSC_CUDA(cudaEventRecord(*e0, s));
 }
 
-void profile_end(cudaStream_t s, cudaEvent_t e0, double bytes) {
+void profile_end(cudaStream_t s, cudaEvent_t e0, double bytes, int64_t launches) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t e1 = take_event();
   CSC_CUDA(cudaEventRecord(e1, s));
-  g_pending.push_back({e0, e1, bytes});
+  g_pending.push_back({e0, e1, bytes, launches});
 }
 
 static void resolve_pending() {
@@ -54,7 +55,7 @@ static void resolve_pending() {
     float ms = 0.f;
     CSC_CUDA(cudaEventElapsedTime(&ms, p.e0, p.e1));
     g_prof.ms += ms;
-    g_prof.launches += 1;
+    g_prof.launches += p.launches;
     g_prof.bytes += p.bytes;
     g_event_pool.push_back(p.e0);
     g_event_pool.push_back(p.e1);
@@ -200,6 +201,7 @@ int csc_set_option(const char* key, int64_t value) {
     if (k == "unroll" && value != 2 && value != 4 && value != 8) fail(CSC_ERR_INVALID, "unroll must be 2, 4 or 8");
     if (k == "l2_persist_pct" && (value < 0 || value > 100)) fail(CSC_ERR_INVALID, "l2_persist_pct in [0, 100]");
     if (k == "persistent" && value != 0 && value != 1) fail(CSC_ERR_INVALID, "persistent must be 0 or 1");
+    if (k == "profile" && (value < 0 || value > 2)) fail(CSC_ERR_INVALID, "profile must be 0, 1 or 2");
     if (k == "lean_mid" && value != 0 && value != 1) fail(CSC_ERR_INVALID, "lean_mid must be 0 or 1");
     if (k == "l2_budget_pct" && (value < 1 || value > 100)) fail(CSC_ERR_INVALID, "l2_budget_pct in [1, 100]");
     slot->store(value);

@@ -138,3 +138,22 @@ def test_lean_mid_step_kernel_matches_general_kernel(filter_golden, dtype):
                 lean = P.apply_filter(low, op, X)
             assert np.array_equal(general, lean), (pw, rec)
             assert relerr(lean, filter_golden["Y_low"]) <= (FP64_TOL if dtype == "float64" else FP32_TOL)
+
+
+def test_profile_modes_count_launches_and_bytes(filter_golden):
+    """profile 1 (per launch) and 2 (per filter span) count the same launches and bytes; the span
+    covers at least the sum of the launches' own times."""
+    from paper_1602_02018_b200 import _lib
+
+    op = c1_op("float32")
+    X = filter_golden["X"]
+    low = P.design_lowpass(0.37, 50)
+    got = {}
+    for mode in (1, 2):
+        _lib.profile_reset()
+        with options(profile=mode):
+            P.apply_filter(low, op, X)
+            got[mode] = _lib.profile_read()
+        _lib.profile_reset()
+    (ms1, n1, b1), (ms2, n2, b2) = got[1], got[2]
+    assert n1 == n2 == 50 and b1 == b2 > 0 and ms1 > 0 and ms2 > 0
