@@ -68,15 +68,15 @@ struct Options {
   std::atomic<int64_t> recurrence{0};     // 0 Clenshaw (4 streams/step), 1 forward (5 streams/step)
   std::atomic<int64_t> cache_hints{1};    // streaming loads evict-first
   std::atomic<int64_t> block_threads{256};
-  std::atomic<int64_t> profile{0};
+  std::atomic<int64_t> profile{0};         // 1: events per step launch, 2: per filter span
   std::atomic<int64_t> l2_budget_pct{50}; // auto panel width: panel gather buffer <= pct% of L2
   std::atomic<int64_t> unroll{4};         // neighbour gathers in flight per lane (4 or 8)
   std::atomic<int64_t> row_order{0};      // 0 interleaved row groups, 1 contiguous ranges per warp
   std::atomic<int64_t> l2_persist_pct{0}; // >0: keep the gathered panel in a persisting L2 window
   std::atomic<int64_t> persistent{1};     // 1: step grid = resident CTAs (grid-stride); 0: one CTA per row block
   std::atomic<int64_t> cg_compact{1};     // block CG: move still-active columns into narrower panels
-  std::atomic<int64_t> cg_overlap{1};     // block CG: a narrower remainder panel runs on a side stream
-  std::atomic<int64_t> lean_mid{1};       // K2: 32-register mid-step kernel (64 warps/SM) for the hot case
+  std::atomic<int64_t> cg_overlap{1};     // block CG: two panels at a time (0 off, 1 auto, 2 no width token)
+  std::atomic<int64_t> lean_mid{1};       // K2: lean mid-step kernel (k_cheb_mid) where it applies
   std::atomic<int64_t> fast_normalize{1}; // K3: vectorised single-panel row normalisation
 };
 extern Options g_opt;
