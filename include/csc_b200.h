@@ -285,6 +285,20 @@ int csc_sbm_edges(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_
                   const int64_t* row_first, const int64_t* col_first, const int64_t* col_size, int64_t capacity,
                   int64_t* src, int64_t* dst, int64_t* num_edges, int64_t* raw_consumed, int device, void* stream);
 
+/* Degree-corrected SBM edges (BASELINE config 4; the reference has no DC-SBM,
+ * SPEC.md:574, so this follows SURVEY.md §8(d)'s spec and stands in for the
+ * reference generator sbm.py:118-155 on that config): independent Bernoulli
+ * edges P(i~j) = min(1, theta_i theta_j q) with q = q_intra inside a community
+ * and q_inter across, drawn in expected O(N + #E) by rejection over geometric
+ * skipping along theta-sorted candidates.  Nodes are community-ordered
+ * (community c owns sizes[c] consecutive ids); theta: N host doubles.  The
+ * edge set depends only on (sizes, theta, q, seed), not on nthreads (<= 0:
+ * all cores).  Host-only.  *num_edges receives the edge count; the edges
+ * (src < dst, host int64) are written only when it is <= capacity. */
+int csc_dcsbm_edges(int64_t num_nodes, int32_t k, const int64_t* sizes, const double* theta, double q_intra,
+                    double q_inter, uint64_t seed, int nthreads, int64_t capacity, int64_t* src, int64_t* dst,
+                    int64_t* num_edges);
+
 /* ---- row-sharded operator (BASELINE config 5) ------------- */
 /* NCCL communicator: rank 0 creates the id, the caller distributes it (e.g. a
  * torch.distributed broadcast), every rank creates its communicator. */

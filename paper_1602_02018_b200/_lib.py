@@ -68,6 +68,7 @@ SIGNATURES: dict[str, list] = {
     "csc_set_exponential_tables": [_p, _p, _p],
     "csc_sbm_edges": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p,
                       _p, _p, _i32, _p],
+    "csc_dcsbm_edges": [_i64, _i32, _p, _p, _f64, _f64, C.c_uint64, _i32, _i64, _p, _p, _p],
     "csc_panel_row_bytes": [_i64, _i32, _i32, _i32, _i64, _p],
     "csc_peers_create": [_i32, _i32, _i32, C.c_size_t, _p],
     "csc_peers_handle": [_p, _p],

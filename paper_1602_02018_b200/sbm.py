@@ -207,16 +207,16 @@ def sbm_generate(cfg: SbmConfig, *, device: int | None = None) -> tuple[Graph, n
 
 
 def dcsbm_edges(cfg: SbmConfig, pareto_alpha: float = 2.5) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
-    """Degree-corrected SBM edges (BASELINE config 4; not in the reference).
+    """Degree-corrected SBM edges (BASELINE config 4; not in the reference, SPEC.md:574).
 
-    Propensities theta_i = 1 + Pareto(alpha) (classical Pareto, x_m = 1),
-    normalised to mean 1 within each community.  Edges follow the Poisson
-    (Karrer-Newman) DC-SBM: the number of edges between communities a <= b is
-    Poisson(q_ab * sum_a(theta) * sum_b(theta)) (halved on the diagonal), with
-    endpoints drawn proportionally to theta inside their community, so that
-    P(i~j) ~= theta_i theta_j q_ab and E[deg_i] = theta_i * avg_degree.
-    Loops are dropped and repeated pairs collapse to one unit-weight edge.
-    Expected O(#E log N) work.
+    SURVEY.md section 8(d)'s spec: propensities theta_i = 1 + Pareto(alpha) (classical
+    Pareto, x_m = 1, ``rng.pareto`` of ``default_rng(cfg.seed)``), normalised to mean 1
+    within each community; independent Bernoulli edges with
+    P(i~j) = min(1, theta_i theta_j q_{c_i c_j}), q = cfg.q1 inside a community and
+    cfg.q2 across (the SbmConfig formulas, sbm.py:60-61), so E[deg_i] ~= theta_i *
+    avg_degree.  The edges are drawn natively (``csc_dcsbm_edges``: rejection over
+    geometric skipping, expected O(N + #E)) from a seed taken from the same generator.
+    Returns (src, dst) sorted with src < dst, the community labels and theta.
     """
     rng = np.random.default_rng(cfg.seed)
     sizes = np.asarray(cfg.sizes, dtype=np.int64)
@@ -224,32 +224,26 @@ def dcsbm_edges(cfg: SbmConfig, pareto_alpha: float = 2.5) -> tuple[np.ndarray, 
     comm = np.repeat(np.arange(cfg.k), sizes)
     theta = 1.0 + rng.pareto(pareto_alpha, size=cfg.num_nodes)
     sums = np.add.reduceat(theta, first[:-1])
-    theta = theta / (sums / sizes)[comm]
-    cum = np.cumsum(theta)
-    lo_c = np.concatenate([[0.0], cum])[first[:-1]]
-    hi_c = cum[first[1:] - 1]
+    theta = np.ascontiguousarray(theta / (sums / sizes)[comm])
+    seed = int(rng.integers(0, 2**63 - 1))
+    n_e = C.c_int64(0)
+    cap = int(cfg.num_nodes * cfg.avg_degree / 2 * 1.1) + 1024
+    for _ in range(2):
+        src = np.empty(cap, dtype=np.int64)
+        dst = np.empty(cap, dtype=np.int64)
+        _lib.call("csc_dcsbm_edges", int(cfg.num_nodes), int(cfg.k), _lib.ptr(sizes), _lib.ptr(theta),
+                  C.c_double(cfg.q1), C.c_double(cfg.q2), C.c_uint64(seed), 0, C.c_int64(cap), _lib.ptr(src), _lib.ptr(dst), C.byref(n_e))
+        if n_e.value <= cap:
+            break
+        cap = int(n_e.value)
+    m = int(n_e.value)
+    order = np.lexsort((dst[:m], src[:m]))
+    return src[:m][order], dst[:m][order], comm, theta
 
-    def draw_in(c: np.ndarray) -> np.ndarray:
-        u = lo_c[c] + rng.random(c.size) * (hi_c[c] - lo_c[c])
-        return np.minimum(np.searchsorted(cum, u, side="right"), first[c + 1] - 1)
 
-    # intra-community edges
-    m_intra = rng.poisson(cfg.q1 * sizes.astype(np.float64) ** 2 / 2.0)
-    ca = np.repeat(np.arange(cfg.k), m_intra)
-    i1, j1 = draw_in(ca), draw_in(ca)
-    # inter-community edges: Poisson thinning of a global theta-weighted process
-    m_all = rng.poisson(cfg.q2 * float(cfg.num_nodes) ** 2 / 2.0)
-    u = rng.random(m_all) * cum[-1]
-    v = rng.random(m_all) * cum[-1]
-    i2 = np.minimum(np.searchsorted(cum, u, side="right"), cfg.num_nodes - 1)
-    j2 = np.minimum(np.searchsorted(cum, v, side="right"), cfg.num_nodes - 1)
-    cross = comm[i2] != comm[j2]
-    i = np.concatenate([i1, i2[cross]])
-    j = np.concatenate([j1, j2[cross]])
-    keep = i != j
-    lo, hi = np.minimum(i[keep], j[keep]), np.maximum(i[keep], j[keep])
-    key = np.unique(lo.astype(np.int64) * cfg.num_nodes + hi)
-    return key // cfg.num_nodes, key % cfg.num_nodes, comm, theta
+def c4_config(seed: int = 0) -> SbmConfig:
+    """BASELINE config 4: N=334,863, k=250, mean degree 5.5, eps = eps_c(5.5, 250)/4."""
+    return SbmConfig(num_nodes=334_863, k=250, avg_degree=5.5, epsilon=critical_epsilon(5.5, 250) / 4.0, seed=seed)
 
 
 def dcsbm_generate(cfg: SbmConfig, pareto_alpha: float = 2.5, *, device: int | None = None):

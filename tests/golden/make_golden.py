@@ -4,7 +4,14 @@ Run in the build container only (the reference lives at /root/reference and is
 not shipped to the GPU box):
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_golden.py [--c2]
+        python tests/golden/make_golden.py [--c2] [--c3] [--c4]
+
+--c3 / --c4 run the reference's run_csc ONCE at the headline configs (C3: SBM N=1e6,
+k=100, d=56, ~1-2 h of one CPU core; C4: the repo's DC-SBM graph, N=334,863, k=250,
+d=51, fed through the reference's build_graph) and capture every stage's output by
+wrapping the stage functions run_csc binds by name (pipeline.py:19-26), the seam the
+reference's own tests monkeypatch (test_pipeline.py:101-110).  Large arrays are stored
+on a fixed row subsample only (features, soft) so the fixtures stay ~1 MB.
 
 Outputs (committed, small): tests/golden/graphs.npz, filter_c1.npz,
 pipeline_c1.npz, formats.npz (the reference's own on-disk formats: feature dump,
@@ -18,6 +25,7 @@ from __future__ import annotations
 import argparse
 import json
 import math
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -102,6 +110,58 @@ def pipeline(N, k, d, seed, full: bool):
     )
     if full:
         out.update(features=feats.rows, soft=res.soft)
+    return out
+
+
+def capture_run(graph, truth, k, d, seed, tag):
+    """run_csc once with every stage's result captured (see module docstring)."""
+    import time
+
+    import cscluster.pipeline as rp
+
+    cap = {}
+
+    def wrap(name):
+        fn = getattr(rp, name)
+
+        def inner(*a, **kw):
+            out = fn(*a, **kw)
+            cap[name] = out
+            return out
+
+        return inner
+
+    saved = {n: getattr(rp, n) for n in ("estimate_lambda_k", "build_features", "draw_sampling", "kmeans",
+                                         "interpolate_all", "generate_signals")}
+    for n in saved:
+        setattr(rp, n, wrap(n))
+    try:
+        op = ref.laplacian_op(graph)
+        t0 = time.perf_counter()
+        res = ref.run_csc(op, ref.CscParams(k=k, d=d, seed=seed))
+        wall = time.perf_counter() - t0
+    finally:
+        for n, fn in saved.items():
+            setattr(rp, n, fn)
+    N = graph.num_nodes
+    est, feats, samp = cap["estimate_lambda_k"], cap["build_features"], cap["draw_sampling"]
+    lab, (soft, info) = cap["kmeans"], cap["interpolate_all"]
+    rows = np.arange(0, N, max(1, N // 512), dtype=np.int64)
+    lab_dtype = np.uint8 if k <= 255 else np.int32
+    out = dict(
+        num_nodes=N, nnz=graph.indptr[-1], trace=np.asarray(est.trace), lambda_k_hat=est.lambda_k_hat,
+        lambda_warning=est.warning, indices=samp.indices, kmeans_labels=lab.labels, kmeans_inertia=lab.inertia,
+        reduced_features=feats.rows[samp.indices], rows=rows, features_rows=feats.rows[rows],
+        soft_rows=soft[rows], soft_colnorm=np.linalg.norm(soft, axis=0),
+        labels=res.labels.astype(lab_dtype), truth=np.asarray(truth).astype(lab_dtype),
+        solver_iterations=info.iterations, solver_residuals=info.residuals, solver_converged=info.converged,
+        ridge=res.diagnostics["ridge"], zero_rows=feats.zero_rows,
+        diagnostics_json=np.frombuffer(json.dumps(res.to_dict()["diagnostics"], sort_keys=True).encode(),
+                                       dtype=np.uint8),
+        ari_truth=ref.adjusted_rand_index(truth, res.labels), timings=json.dumps(res.diagnostics["timings"]),
+        wall_s=wall,
+    )
+    print(tag, "wall", round(wall, 1), "s", json.dumps(res.diagnostics["timings"]), flush=True)
     return out
 
 
@@ -210,7 +270,29 @@ def edgelists():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
+    ap.add_argument("--c3", action="store_true")
+    ap.add_argument("--c4", action="store_true")
+    ap.add_argument("--only", action="store_true", help="skip the small fixtures")
     args = ap.parse_args()
+    if args.c3:
+        N, k = 1_000_000, 100
+        g, truth = ref.sbm_generate(sbm_config(N, k))
+        out = capture_run(g, truth, k, int(math.ceil(4 * math.log(N))), 0, "c3")
+        np.savez_compressed(OUT / "pipeline_c3.npz", **out)
+    if args.c4:
+        sys.path.insert(0, str(OUT.parents[1]))
+        from paper_1602_02018_b200.sbm import c4_config, dcsbm_edges
+
+        cfg = c4_config()
+        src, dst, truth, _ = dcsbm_edges(cfg)
+        edges = np.column_stack([src, dst, np.ones(src.size)]).astype(np.float64)
+        g = ref.build_graph(edges, num_nodes=cfg.num_nodes)
+        out = capture_run(g, truth, cfg.k, int(math.ceil(4 * math.log(cfg.num_nodes))), 0, "c4")
+        out["edges_digest"] = np.frombuffer(__import__("hashlib").sha256(
+            np.ascontiguousarray(np.column_stack([src, dst]).astype(np.int64)).tobytes()).digest(), dtype=np.uint8)
+        np.savez_compressed(OUT / "pipeline_c4.npz", **out)
+    if args.only:
+        return
     graphs()
     filter_c1()
     formats()
