@@ -1,6 +1,7 @@
 // K2 implementation: fused Chebyshev step kernel, panel planning, packing, and
 // the filter-level C-ABI entry points (Laplacian apply, filter, eigencount,
 // features).  See filter.cuh for the formulation.
+#include <atomic>
 #include <algorithm>
 #include <chrono>
 #include <mutex>
@@ -473,12 +474,16 @@ template <typename T, int LPR, int MINB = (LPR == 16 ? 6 : 8)>
 static int launch_mid(const StepArgs& a, int device, cudaStream_t s) {
   const bool unit = a.wv == nullptr;
   auto kern = unit ? k_cheb_mid<T, LPR, MINB, true> : k_cheb_mid<T, LPR, MINB, false>;
-  static int occ_cache[2] = {0, 0};  // [unit]
-  int& occ = occ_cache[unit ? 1 : 0];
+  // per (device, unit) occupancy, published atomically: concurrent host threads (the CG
+  // overlap worker) either see 0 and compute the same value or read the stored one
+  static std::atomic<int> occ_cache[64][2];
+  std::atomic<int>& slot = occ_cache[device & 63][unit ? 1 : 0];
+  int occ = slot.load(std::memory_order_acquire);
   if (occ == 0) {
     int o = 0;
     CSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, 0));
     occ = std::max(o, 1);
+    slot.store(occ, std::memory_order_release);
   }
   const int64_t rows_per_block = 8 * (32 / LPR);
   const int64_t need = (a.n + rows_per_block - 1) / rows_per_block;

@@ -82,3 +82,39 @@ def test_deterministic_and_refine(c1_golden):
     plain = P.estimate_lambda_k(c1_op(), 20, rng=np.random.default_rng(9))
     ref = P.estimate_lambda_k(c1_op(), 20, rng=np.random.default_rng(9), refine=True)
     assert ref.lambda_k_hat <= plain.lambda_k_hat
+
+
+def test_fp32_guard_reprobes_in_fp64(c1_golden, monkeypatch):
+    """Every probe inside the (widened) guard band is re-run in fp64 on the same block:
+    the trace then equals the fp64 trace bit for bit (spectrum.py:49-50, 125-137)."""
+    from paper_1602_02018_b200 import spectrum as S
+
+    e64 = P.estimate_lambda_k(c1_op(), 20, rng=substream(0, "probe"))
+    monkeypatch.setattr(S, "FP32_GUARD_RTOL", 10.0)
+    e32 = P.estimate_lambda_k(c1_op("float32"), 20, rng=substream(0, "probe"))
+    assert e32.fp64_reprobes == list(range(len(e32.trace)))
+    assert e32.trace == e64.trace and e32.lambda_k_hat == e64.lambda_k_hat
+    # fp64 operators never re-probe; the default band leaves C1's probes alone
+    assert e64.fp64_reprobes == []
+    monkeypatch.setattr(S, "FP32_GUARD_RTOL", 1e-5)
+    plain = P.estimate_lambda_k(c1_op("float32"), 20, rng=substream(0, "probe"))
+    assert plain.lambda_k_hat == float(c1_golden["lambda_k_hat"])
+
+
+def test_fp32_guard_boundary_predicate():
+    from paper_1602_02018_b200.spectrum import near_decision_boundary
+
+    assert near_decision_boundary(19.5004, 20) and near_decision_boundary(20.4996, 20)
+    assert not near_decision_boundary(19.51, 20) and not near_decision_boundary(20.0, 20)
+    assert not near_decision_boundary(45_850.5, 20)  # far from k: cannot flip a decision
+
+
+def test_fp32_guard_in_run_csc_diagnostics(monkeypatch):
+    from paper_1602_02018_b200 import spectrum as S
+
+    monkeypatch.setattr(S, "FP32_GUARD_RTOL", 10.0)
+    r32 = P.run_csc(c1_op("float32"), P.CscParams(k=20, d=28, seed=0))
+    r64 = P.run_csc(c1_op(), P.CscParams(k=20, d=28, seed=0))
+    assert r32.diagnostics["probe_fp64_reprobes"] == list(range(r32.diagnostics["probe_iterations"]))
+    assert "probe_fp64_reprobes" not in r64.diagnostics
+    assert r32.diagnostics["lambda_k_hat"] == r64.diagnostics["lambda_k_hat"]
