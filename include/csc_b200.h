@@ -306,12 +306,17 @@ int csc_comm_unique_id(uint8_t* out /* CSC_UNIQUE_ID_BYTES */);
 int csc_comm_create(const uint8_t* unique_id, int nranks, int rank, int device, csc_comm** out);
 int csc_comm_destroy(csc_comm* comm);
 
-/* This rank's rows [row_begin, row_begin + num_rows) of an N-node graph as a
- * CSR with global column indices (indptr local, starting at 0).  Ranks own
- * R = ceil(N / nranks) consecutive rows each (the last may own fewer). */
-int csc_graph_create_rows(int64_t num_nodes, int64_t row_begin, int64_t num_rows, int64_t nnz,
-                          const int32_t* indptr, const int32_t* indices, const double* weights, int dtype,
-                          int device, void* stream, csc_graph** out);
+/* Rank `rank`'s row shard of an N-node graph: rows [row_starts[rank],
+ * row_starts[rank + 1]) as a CSR (indptr local, starting at 0; indices = global
+ * node ids, host arrays).  row_starts (nranks + 1 entries, 0 .. N, non-decreasing)
+ * is any contiguous partition -- dist.row_partition balances it by nnz (SURVEY.md
+ * §8e).  The gather panel every step reads holds nranks slots of
+ * R = max_q (row_starts[q+1] - row_starts[q]) rows, rank q's rows at q R (the
+ * all-gather of equal R-row chunks); the shard's column indices are remapped to
+ * those panel rows here. */
+int csc_graph_create_row_shard(int64_t num_nodes, int nranks, int rank, const int64_t* row_starts, int64_t nnz,
+                               const int32_t* indptr, const int32_t* indices, const double* weights, int dtype,
+                               int device, void* stream, csc_graph** out);
 
 /* Chebyshev filter on a row-sharded block (X, Y: this rank's rows, device
  * buffers): every step is followed by an ncclAllGather of the step's rows into
@@ -321,6 +326,17 @@ int csc_graph_create_rows(int64_t num_nodes, int64_t row_begin, int64_t num_rows
 int csc_cheb_filter_rows(const csc_graph* g, csc_comm* comm, const double* coeffs, int ncoeffs, const void* X,
                          int64_t ldx, void* Y, int64_t ldy, int ncols, int io_dtype, int mode, double* out,
                          void* stream);
+
+/* Every rank's row shard in ONE process on one device, stepped in lockstep with
+ * the all-gather done as device copies into the shared gather panel: the
+ * single-GPU execution of the multi-rank row-sharded filter (same kernels, same
+ * per-rank arguments and panel layout as csc_cheb_filter_rows; ranks that wait on
+ * one another cannot share a GPU, so this is how nranks > 1 runs on one device).
+ * shards[q] must be rank q's shard; X[q] / Y[q] / out[q] are rank q's blocks and
+ * results (modes as csc_cheb_filter_rows). */
+int csc_cheb_filter_rows_group(const csc_graph* const* shards, int nshards, const double* coeffs, int ncoeffs,
+                               const void* const* X, const int64_t* ldx, void* const* Y, const int64_t* ldy, int ncols,
+                               int io_dtype, int mode, double* const* out, void* stream);
 
 /* Peer-memory transport (the all-gather fused into the step kernel over NVLink):
  * csc_peers_create allocates this rank's two gather panels of panel_bytes each

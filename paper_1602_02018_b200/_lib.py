@@ -78,7 +78,8 @@ SIGNATURES: dict[str, list] = {
     "csc_comm_unique_id": [_p],
     "csc_comm_create": [_p, _i32, _i32, _i32, _p],
     "csc_comm_destroy": [_p],
-    "csc_graph_create_rows": [_i64, _i64, _i64, _i64, _p, _p, _p, _i32, _i32, _p, _p],
+    "csc_graph_create_row_shard": [_i64, _i32, _i32, _p, _i64, _p, _p, _p, _i32, _i32, _p, _p],
+    "csc_cheb_filter_rows_group": [_p, _i32, _p, _i32, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p],
     "csc_cheb_filter_rows": [_p, _p, _p, _i32, _p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p],
     "csc_assign_partial": [_p, _i64, _i64, _i32, _i32, _i64, _p, _p, _p, _p, _i32, _p],
 }

@@ -604,7 +604,9 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   a.contig = g_opt.row_order.load() == 1;
   constexpr int VEC = 16 / sizeof(T);
   const int lpr = pw / VEC;
-  if (a.n > 0 && (uint64_t)a.n * (uint64_t)lpr >= (1ull << 32))
+  // rows of the gathered panel: the local rows, or every rank's slots of a row shard
+  const int64_t gsrc = std::max<int64_t>(a.n, g->gather_rows);
+  if (gsrc > 0 && (uint64_t)gsrc * (uint64_t)lpr >= (1ull << 32))
     fail(CSC_ERR_INVALID, "panel too large for 32-bit vector offsets (rows x lanes >= 2^32)");
   const int threads = (int)g_opt.block_threads.load();
   const bool prof = g_opt.profile.load() == 1 && a.G != nullptr;  // 2: per filter span (filter_panel)
@@ -622,7 +624,7 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
                     a.npeers == 0 && a.G != nullptr && a.O != nullptr && !a.contig && threads == 256 &&
                     g_opt.unroll.load() == 4 && g_opt.persistent.load() && persist_bytes(g->device) == 0 &&
                     lpr != 2 &&
-                    (double)a.n * lpr * 16.0 <= 4.0 * (double)device_props(g->device).l2_bytes;
+                    (double)gsrc * lpr * 16.0 <= 4.0 * (double)device_props(g->device).l2_bytes;
   if (lean) {
     switch (lpr) {
       case 1: grid = launch_mid<T, 1>(a, g->device, s); break;

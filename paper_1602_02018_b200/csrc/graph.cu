@@ -194,6 +194,7 @@ csc_graph* graph_from_device_csr(int64_t n, int64_t nnz, int32_t* indptr, int32_
   g->indices = indices;
   g->weights = weights;
   g->n_global = n;
+  g->gather_rows = n;
   try {
     const size_t es = dtype_size(dtype);
     CSC_CUDA(cudaMalloc(&g->degrees, sizeof(double) * (n > 0 ? n : 1)));

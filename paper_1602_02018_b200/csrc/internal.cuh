@@ -267,6 +267,12 @@ struct csc_graph {
   bool unit = false;
   int64_t n_global = 0;   // columns / global nodes (== n unless row-sharded)
   int64_t row_begin = 0;  // first global row held (row-sharded operators)
+  // row shards (rows.cu): the gather panel holds shard_ranks slots of shard_R rows (rank q's
+  // rows at q * shard_R), and `indices` are panel rows, not node ids.  Replicated: 0 / 0.
+  int shard_ranks = 0;
+  int shard_rank = 0;
+  int64_t shard_R = 0;
+  int64_t gather_rows = 0;  // rows of the panel a step gathers from (n, or shard_ranks * shard_R)
 };
 
 namespace csc {

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -101,110 +102,130 @@ struct csc_peers {
 namespace csc {
 namespace rows_impl {
 
-// per-rank row range of an N-row block over `nranks` (equal counts; the last rank may be short)
-int64_t rows_per_rank(int64_t n, int nranks) { return (n + nranks - 1) / nranks; }
+// One Clenshaw filter (the recurrence of filter_panel, filters.py:140-155) as a list of
+// steps over named per-rank buffers, shared by the three exchanges below: every step but the
+// last is followed by an all-gather of its output rows into the next gather panel, and the
+// scaled input Xs is all-gathered before the first step (when p >= 1).
+enum Buf : int { B_NONE = 0, B_X, B_XS, B_Y, B_0, B_1 };
 
-template <typename T>
-void filter_panel_rows(const csc_graph* g, csc_comm* cm, const double* c, int nc, const T* X, const T* Xs, T* Y,
-                       T* B0, T* B1, T* F, int64_t R, int pw, int wc, int epi, double* part, cudaStream_t s) {
+struct PlanStep {
+  double ka = 0.0, ks = 0.0, kx = 0.0;
+  Buf S = B_NONE, X = B_NONE, O = B_NONE;
+  bool gather = false;  // G = the current gather panel
+  bool last = false;
+};
+
+std::vector<PlanStep> clenshaw_plan(const double* c, int nc) {
   const int p = nc - 1;
-  double hz = 0.0;
-  for (int l = 0; l < nc; l += 2) hz += ((l / 2) % 2 ? -c[l] : c[l]);
-  const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-  auto gather = [&](const T* local) {  // local R x pw rows -> full (nranks R) x pw panel
-    CSC_NCCL(nccl().allGather(local, F, (size_t)R * pw, dt, cm->comm, s));
-  };
-  auto base = [&]() {
-    StepArgs a{};
-    a.indptr = g->indptr;
-    a.indices = g->indices;
-    a.wv = g->wv;
-    a.rs = g->rs;
-    a.n = g->n;  // local rows
-    a.wc = wc;
-    a.hz = hz;
-    return a;
-  };
-  auto run = [&](StepArgs a, int e) {
-    if (e != EPI_NONE) {
-      a.part = part;
-      a.last = 1;
-    }
-    launch_step<T>(g, a, pw, e, s);
+  std::vector<PlanStep> v;
+  auto step = [&](bool G, double ka, Buf S, double ks, Buf X, double kx, Buf O, bool last) {
+    PlanStep t;
+    t.gather = G;
+    t.ka = ka;
+    t.S = S;
+    t.ks = ks;
+    t.X = X;
+    t.kx = kx;
+    t.O = O;
+    t.last = last;
+    v.push_back(t);
   };
   if (p == 0) {
-    StepArgs a = base();
-    a.X = X;
-    a.kx = c[0];
-    a.O = Y;
-    a.last = 1;
-    run(a, epi);
-    return;
+    step(false, 0.0, B_NONE, 0.0, B_X, c[0], B_Y, true);
+    return v;
   }
-  gather(Xs);
   if (p == 1) {
-    StepArgs a = base();
-    a.G = F;
-    a.ka = -c[1];
-    a.X = X;
-    a.kx = c[0];
-    a.O = Y;
-    a.last = 1;
-    run(a, epi);
-    return;
+    step(true, -c[1], B_NONE, 0.0, B_X, c[0], B_Y, true);
+    return v;
   }
-  StepArgs a = base();
-  a.G = F;
-  a.ka = -2.0 * c[p];
-  a.X = Xs;
-  a.kx = c[p - 1];
-  a.O = B0;
-  run(a, EPI_NONE);
-  gather(B0);
+  step(true, -2.0 * c[p], B_NONE, 0.0, B_XS, c[p - 1], B_0, false);
   if (p == 2) {
-    StepArgs f = base();
-    f.G = F;
-    f.ka = -1.0;
-    f.X = X;
-    f.kx = c[0] - c[2];
-    f.O = Y;
-    f.last = 1;
-    run(f, epi);
-    return;
+    step(true, -1.0, B_NONE, 0.0, B_X, c[0] - c[2], B_Y, true);
+    return v;
   }
-  StepArgs b = base();
-  b.G = F;
-  b.ka = -2.0;
-  b.X = Xs;
-  b.kx = c[p - 2] - c[p];
-  b.O = B1;
-  run(b, EPI_NONE);
-  gather(B1);
-  T* cur = B1;
-  T* prv = B0;
-  for (int l = p - 3; l >= 1; --l) {
-    StepArgs m = base();
-    m.G = F;
-    m.ka = -2.0;
-    m.S = prv;
-    m.ks = -1.0;
-    m.X = Xs;
-    m.kx = c[l];
-    m.O = prv;
-    run(m, EPI_NONE);
-    gather(prv);
+  step(true, -2.0, B_NONE, 0.0, B_XS, c[p - 2] - c[p], B_1, false);
+  Buf prv = B_0, cur = B_1;
+  for (int l = p - 3; l >= 1; --l) {  // in place: b_l overwrites b_{l+2}
+    step(true, -2.0, prv, -1.0, B_XS, c[l], prv, false);
     std::swap(cur, prv);
   }
-  StepArgs f = base();
-  f.G = F;
-  f.ka = -1.0;
-  f.S = prv;
-  f.ks = -1.0;
-  f.X = X;
-  f.kx = c[0];
-  f.O = Y;
-  f.last = 1;
-  run(f, epi);
+  step(true, -1.0, prv, -1.0, B_X, c[0], B_Y, true);
+  return v;
+}
+
+double filter_hz(const double* c, int nc) {  // h(1): the filter on isolated nodes
+  double hz = 0.0;
+  for (int l = 0; l < nc; l += 2) hz += ((l / 2) % 2 ? -c[l] : c[l]);
+  return hz;
+}
+
+// one rank's R x pw panels of one column panel
+struct RankPanels {
+  const csc_graph* g = nullptr;
+  void* buf[6] = {};  // indexed by Buf
+  double* part = nullptr;
+  template <typename T>
+  T* at(Buf b) const { return static_cast<T*>(buf[b]); }
+};
+
+template <typename T>
+StepArgs plan_args(const RankPanels& rp, const PlanStep& st, const void* G, int wc, double hz, int epi) {
+  StepArgs a{};
+  const csc_graph* g = rp.g;
+  a.indptr = g->indptr;
+  a.indices = g->indices;
+  a.wv = g->wv;
+  a.rs = g->rs;
+  a.n = g->n;  // local rows
+  a.wc = wc;
+  a.hz = hz;
+  a.G = st.gather ? G : nullptr;
+  a.ka = st.ka;
+  a.S = st.S ? rp.at<T>(st.S) : nullptr;
+  a.ks = st.ks;
+  a.X = rp.at<T>(st.X);
+  a.kx = st.kx;
+  a.O = rp.at<T>(st.O);
+  a.last = st.last ? 1 : 0;
+  if (st.last && epi != EPI_NONE) a.part = rp.part;
+  return a;
+}
+
+// NCCL: every rank runs the plan on its own stream; ncclAllGather after each step.
+template <typename T>
+void filter_panel_nccl(csc_comm* cm, const RankPanels& rp, const double* c, int nc, T* F, int64_t R, int pw, int wc,
+                       int epi, cudaStream_t s) {
+  const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+  auto gather = [&](Buf b) {  // local R x pw rows -> full (nranks R) x pw panel
+    CSC_NCCL(nccl().allGather(rp.at<T>(b), F, (size_t)R * pw, dt, cm->comm, s));
+  };
+  const double hz = filter_hz(c, nc);
+  if (nc > 1) gather(B_XS);
+  for (const PlanStep& st : clenshaw_plan(c, nc)) {
+    launch_step<T>(rp.g, plan_args<T>(rp, st, F, wc, hz, epi), pw, st.last ? epi : EPI_NONE, s);
+    if (!st.last) gather(st.O);
+  }
+}
+
+// Emulated ranks (one process, one device): the shards step in lockstep on one stream and the
+// all-gather is a device copy of each shard's R rows into its slot of the shared panel -- the
+// multi-rank exchange without ranks that wait on one another (B200_PROFILING.md).  Same kernels,
+// same per-rank arguments, same panel layout as the NCCL path.
+template <typename T>
+void filter_panel_group(const std::vector<RankPanels>& ranks, const double* c, int nc, T* F, int64_t R, int pw,
+                        int wc, int epi, cudaStream_t s) {
+  auto gather = [&](Buf b) {
+    for (size_t q = 0; q < ranks.size(); ++q)
+      CSC_CUDA(cudaMemcpyAsync(F + (size_t)q * R * pw, ranks[q].at<T>(b), sizeof(T) * (size_t)R * pw,
+                               cudaMemcpyDeviceToDevice, s));
+  };
+  const double hz = filter_hz(c, nc);
+  if (nc > 1) gather(B_XS);
+  for (const PlanStep& st : clenshaw_plan(c, nc)) {
+    for (const RankPanels& rp : ranks)
+      launch_step<T>(rp.g, plan_args<T>(rp, st, F, wc, hz, epi), pw, st.last ? epi : EPI_NONE, s);
+    if (!st.last) gather(st.O);
+  }
 }
 
 // every rank publishes `epoch` in its slot of every rank's flag array, then waits
@@ -243,108 +264,34 @@ void peer_put(csc_peers* pe, int which, const T* local, int64_t R, int pw, cudaS
     CSC_CUDA(cudaMemcpyAsync(static_cast<char*>(pe->peer[q]) + off, local, bytes, cudaMemcpyDeviceToDevice, s));
 }
 
+// Peer transport: the all-gather fused into each non-last step (its epilogue stores the
+// step's rows into every rank's other panel), a flag barrier after it.
 template <typename T>
-void filter_panel_peers(const csc_graph* g, csc_peers* pe, const double* c, int nc, const T* X, const T* Xs, T* Y,
-                        T* B0, T* B1, int64_t R, int pw, int wc, int epi, double* part, cudaStream_t s) {
-  const int p = nc - 1;
-  double hz = 0.0;
-  for (int l = 0; l < nc; l += 2) hz += ((l / 2) % 2 ? -c[l] : c[l]);
-  int cur_panel = 0;  // gather source of the next step
-  auto panel = [&](int which) { return static_cast<T*>(static_cast<void*>(static_cast<char*>(pe->base) +
-                                                                          (size_t)which * pe->stride)); };
-  auto base = [&]() {
-    StepArgs a{};
-    a.indptr = g->indptr;
-    a.indices = g->indices;
-    a.wv = g->wv;
-    a.rs = g->rs;
-    a.n = g->n;  // local rows
-    a.wc = wc;
-    a.hz = hz;
-    return a;
+void filter_panel_peers(csc_peers* pe, const RankPanels& rp, const double* c, int nc, int64_t R, int pw, int wc,
+                        int epi, cudaStream_t s) {
+  const double hz = filter_hz(c, nc);
+  auto panel = [&](int which) {
+    return static_cast<T*>(static_cast<void*>(static_cast<char*>(pe->base) + (size_t)which * pe->stride));
   };
-  // a mid step: gather panel cur, O = local rows, fused stores into every rank's other panel
-  auto mid = [&](StepArgs a) {
-    a.G = panel(cur_panel);
+  int cur_panel = 0;  // gather source of the next step
+  if (nc > 1) {
+    peer_barrier(pe, s);  // every rank is done with the previous call's panels
+    peer_put<T>(pe, 0, rp.at<T>(B_XS), R, pw, s);
+    peer_barrier(pe, s);
+  }
+  for (const PlanStep& st : clenshaw_plan(c, nc)) {
+    StepArgs a = plan_args<T>(rp, st, panel(cur_panel), wc, hz, epi);
+    if (st.last) {
+      launch_step<T>(rp.g, a, pw, epi, s);
+      continue;
+    }
     a.peers = pe->dptrs + (size_t)(1 - cur_panel) * pe->nranks;
     a.npeers = pe->nranks;
     a.peer_row0 = (int64_t)pe->rank * R;
-    launch_step<T>(g, a, pw, EPI_NONE, s);
+    launch_step<T>(rp.g, a, pw, EPI_NONE, s);
     peer_barrier(pe, s);
     cur_panel = 1 - cur_panel;
-  };
-  auto last = [&](StepArgs a) {
-    a.G = a.G ? panel(cur_panel) : nullptr;
-    a.last = 1;
-    if (epi != EPI_NONE) a.part = part;
-    launch_step<T>(g, a, pw, epi, s);
-  };
-  if (p == 0) {
-    StepArgs a = base();
-    a.X = X;
-    a.kx = c[0];
-    a.O = Y;
-    last(a);
-    return;
   }
-  peer_barrier(pe, s);  // every rank is done with the previous call's panels
-  peer_put<T>(pe, 0, Xs, R, pw, s);
-  peer_barrier(pe, s);
-  cur_panel = 0;
-  if (p == 1) {
-    StepArgs a = base();
-    a.G = Xs;  // placeholder: replaced by the gather panel
-    a.ka = -c[1];
-    a.X = X;
-    a.kx = c[0];
-    a.O = Y;
-    last(a);
-    return;
-  }
-  StepArgs a = base();
-  a.ka = -2.0 * c[p];
-  a.X = Xs;
-  a.kx = c[p - 1];
-  a.O = B0;
-  mid(a);
-  if (p == 2) {
-    StepArgs f = base();
-    f.G = Xs;
-    f.ka = -1.0;
-    f.X = X;
-    f.kx = c[0] - c[2];
-    f.O = Y;
-    last(f);
-    return;
-  }
-  StepArgs b = base();
-  b.ka = -2.0;
-  b.X = Xs;
-  b.kx = c[p - 2] - c[p];
-  b.O = B1;
-  mid(b);
-  T* prv = B0;
-  T* cur = B1;
-  for (int l = p - 3; l >= 1; --l) {
-    StepArgs m = base();
-    m.ka = -2.0;
-    m.S = prv;
-    m.ks = -1.0;
-    m.X = Xs;
-    m.kx = c[l];
-    m.O = prv;
-    mid(m);
-    std::swap(cur, prv);
-  }
-  StepArgs f = base();
-  f.G = Xs;
-  f.ka = -1.0;
-  f.S = prv;
-  f.ks = -1.0;
-  f.X = X;
-  f.kx = c[0];
-  f.O = Y;
-  last(f);
 }
 
 template <typename Ti, typename To>
@@ -372,48 +319,82 @@ __global__ void k_unpack_rows(const Ti* __restrict__ src, int c0, int wc, int pw
   }
 }
 
-// one of cm (NCCL all-gather after each step) / pe (peer stores fused into the step)
+// Per-rank scratch of one filter call: packed input (symmetric and scaled), output and the
+// two recurrence panels, R x max_pw each, zeroed so the pad rows a rank sends are zeros.
+struct RankScratch {
+  Scratch x, xs, y, b0, b1, part;
+  RankScratch(size_t panel_bytes, size_t part_bytes, cudaStream_t s)
+      : x(panel_bytes, s), xs(panel_bytes, s), y(panel_bytes, s), b0(panel_bytes, s), b1(panel_bytes, s),
+        part(part_bytes, s) {
+    for (Scratch* b : {&x, &xs, &y, &b0, &b1}) CSC_CUDA(cudaMemsetAsync(b->get(), 0, b->bytes(), s));
+  }
+};
+
+// One rank's call (NCCL or peers) or all emulated ranks' calls (group): pack, run every column
+// panel's plan, unpack; mode 0 Y = h(L) X, 1 sum of squares per rank, 2 Y + row sums of squares.
 template <typename T, typename Tio>
-void run_rows(const csc_graph* g, csc_comm* cm, csc_peers* pe, const double* coeffs, int nc, const Tio* X,
-              int64_t ldx, Tio* Y, int64_t ldy, int ncols, int mode, double* count_or_rowsq, cudaStream_t s) {
-  const int64_t n = g->n;
-  const int nranks = pe ? pe->nranks : cm->nranks;
-  const int64_t R = rows_per_rank(g->n_global, nranks);
-  const PanelPlan pp = plan_panels(g->n_global, ncols, g->dtype, g->device, g->nnz * nranks);
+void run_rows(const std::vector<const csc_graph*>& gs, csc_comm* cm, csc_peers* pe, const double* coeffs, int nc,
+              const std::vector<const Tio*>& X, const std::vector<int64_t>& ldx, const std::vector<Tio*>& Y,
+              const std::vector<int64_t>& ldy, int ncols, int mode, const std::vector<double*>& outs,
+              cudaStream_t s) {
+  const csc_graph* g0 = gs[0];
+  const int nranks = g0->shard_ranks;
+  const int64_t R = g0->shard_R;
+  int64_t nnz_all = 0;
+  for (const csc_graph* g : gs) nnz_all += g->nnz;
+  if (gs.size() == 1) nnz_all = g0->nnz * nranks;  // one rank of many: estimate
+  const PanelPlan pp = plan_panels(g0->gather_rows, ncols, g0->dtype, g0->device, nnz_all);
   if (pe && sizeof(T) * (size_t)R * nranks * pp.max_pw > pe->panel_bytes)
     fail(CSC_ERR_INVALID, "peer panels too small for this block (see csc_panel_row_bytes)");
-  const int cap = step_grid_cap(g->device);
-  Scratch x(sizeof(T) * R * pp.max_pw, s), xs(sizeof(T) * R * pp.max_pw, s), y(sizeof(T) * R * pp.max_pw, s),
-      b0(sizeof(T) * R * pp.max_pw, s), b1(sizeof(T) * R * pp.max_pw, s),
-      full(pe ? 16 : sizeof(T) * (size_t)R * nranks * pp.max_pw, s);
-  Scratch part(sizeof(double) * std::max<int64_t>((int64_t)cap * pp.np, n), s);
-  CSC_CUDA(cudaMemsetAsync(x.get(), 0, x.bytes(), s));
-  CSC_CUDA(cudaMemsetAsync(xs.get(), 0, xs.bytes(), s));
-  CSC_CUDA(cudaMemsetAsync(b0.get(), 0, b0.bytes(), s));
-  CSC_CUDA(cudaMemsetAsync(b1.get(), 0, b1.bytes(), s));
-  if (mode == 1) CSC_CUDA(cudaMemsetAsync(part.get(), 0, part.bytes(), s));
-  if (mode == 2) CSC_CUDA(cudaMemsetAsync(count_or_rowsq, 0, sizeof(double) * n, s));
+  const int cap = step_grid_cap(g0->device);
+  const size_t pbytes = sizeof(T) * (size_t)R * pp.max_pw;
+  std::vector<std::unique_ptr<RankScratch>> sc;
+  for (const csc_graph* g : gs)
+    sc.emplace_back(new RankScratch(pbytes, sizeof(double) * std::max<int64_t>((int64_t)cap * pp.np, g->n), s));
+  Scratch full(pe ? 16 : sizeof(T) * (size_t)R * nranks * pp.max_pw, s);
+  for (size_t q = 0; q < gs.size(); ++q) {
+    if (mode == 1) CSC_CUDA(cudaMemsetAsync(sc[q]->part.get(), 0, sc[q]->part.bytes(), s));
+    if (mode == 2) CSC_CUDA(cudaMemsetAsync(outs[q], 0, sizeof(double) * gs[q]->n, s));
+  }
+  const int epi = mode == 1 ? EPI_SUMSQ : (mode == 2 ? EPI_ROWSQ : EPI_NONE);
   for (int j = 0; j < pp.np; ++j) {
     const int pw = pp.pw[j], wc = pp.wc[j];
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n * pw + 255) / 256, 148 * 64));
-    k_pack_rows<Tio, T><<<grid, 256, 0, s>>>(X, ldx, pp.c0[j], wc, pw, n, g->dis, x.as<T>(), xs.as<T>());
-    CSC_LAUNCHED();
-    const int epi = mode == 1 ? EPI_SUMSQ : (mode == 2 ? EPI_ROWSQ : EPI_NONE);
-    double* pj = mode == 1 ? part.as<double>() + (size_t)cap * j : part.as<double>();
-    if (pe)
-      filter_panel_peers<T>(g, pe, coeffs, nc, x.as<T>(), xs.as<T>(), mode == 1 ? nullptr : y.as<T>(), b0.as<T>(),
-                            b1.as<T>(), R, pw, wc, epi, pj, s);
-    else
-      filter_panel_rows<T>(g, cm, coeffs, nc, x.as<T>(), xs.as<T>(), mode == 1 ? nullptr : y.as<T>(), b0.as<T>(),
-                           b1.as<T>(), full.as<T>(), R, pw, wc, epi, pj, s);
-    if (mode != 1) {
-      k_unpack_rows<T, Tio><<<(int)std::max<int64_t>(1, std::min<int64_t>((n * wc + 255) / 256, 148 * 64)), 256, 0,
-                              s>>>(y.as<T>(), pp.c0[j], wc, pw, n, Y, ldy, part.as<double>(),
-                                   mode == 2 ? count_or_rowsq : nullptr);
+    std::vector<RankPanels> rps(gs.size());
+    for (size_t q = 0; q < gs.size(); ++q) {
+      const csc_graph* g = gs[q];
+      const int64_t n = g->n;
+      RankScratch& r = *sc[q];
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n * pw + 255) / 256, 148 * 64));
+      k_pack_rows<Tio, T><<<grid, 256, 0, s>>>(X[q], ldx[q], pp.c0[j], wc, pw, n, g->dis, r.x.as<T>(), r.xs.as<T>());
       CSC_LAUNCHED();
+      RankPanels& rp = rps[q];
+      rp.g = g;
+      rp.buf[B_X] = r.x.get();
+      rp.buf[B_XS] = r.xs.get();
+      rp.buf[B_Y] = mode == 1 ? nullptr : r.y.get();  // SUMSQ: the partials only
+      rp.buf[B_0] = r.b0.get();
+      rp.buf[B_1] = r.b1.get();
+      rp.part = mode == 1 ? r.part.as<double>() + (size_t)cap * j : (mode == 2 ? r.part.as<double>() : nullptr);
+    }
+    if (pe)
+      filter_panel_peers<T>(pe, rps[0], coeffs, nc, R, pw, wc, epi, s);
+    else if (cm)
+      filter_panel_nccl<T>(cm, rps[0], coeffs, nc, full.as<T>(), R, pw, wc, epi, s);
+    else
+      filter_panel_group<T>(rps, coeffs, nc, full.as<T>(), R, pw, wc, epi, s);
+    if (mode == 0 || mode == 2) {
+      for (size_t q = 0; q < gs.size(); ++q) {
+        const int64_t n = gs[q]->n;
+        k_unpack_rows<T, Tio><<<(int)std::max<int64_t>(1, std::min<int64_t>((n * wc + 255) / 256, 148 * 64)), 256,
+                                0, s>>>(sc[q]->y.as<T>(), pp.c0[j], wc, pw, n, Y[q], ldy[q], sc[q]->part.as<double>(),
+                                        mode == 2 ? outs[q] : nullptr);
+        CSC_LAUNCHED();
+      }
     }
   }
-  if (mode == 1) reduce_sum(part.as<double>(), (int64_t)cap * pp.np, count_or_rowsq, s);
+  if (mode == 1)
+    for (size_t q = 0; q < gs.size(); ++q)
+      reduce_sum(sc[q]->part.as<double>(), (int64_t)cap * pp.np, outs[q], s);
 }
 
 }  // namespace rows_impl
@@ -461,18 +442,39 @@ int csc_comm_destroy(csc_comm* c) {
   });
 }
 
-int csc_graph_create_rows(int64_t num_nodes, int64_t row_begin, int64_t num_rows, int64_t nnz, const int32_t* indptr,
-                          const int32_t* indices, const double* weights, int dtype, int device, void* stream,
-                          csc_graph** out) {
+int csc_graph_create_row_shard(int64_t num_nodes, int nranks, int rank, const int64_t* row_starts, int64_t nnz,
+                               const int32_t* indptr, const int32_t* indices, const double* weights, int dtype,
+                               int device, void* stream, csc_graph** out) {
   return guard([&] {
-    if (!out || !indptr) fail(CSC_ERR_INVALID, "NULL argument");
-    if (row_begin < 0 || num_rows < 0 || row_begin + num_rows > num_nodes) fail(CSC_ERR_INVALID, "bad row range");
+    if (!out || !indptr || !row_starts) fail(CSC_ERR_INVALID, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(CSC_ERR_INVALID, "bad rank / nranks");
     if (dtype != CSC_F64 && dtype != CSC_F32) fail(CSC_ERR_INVALID, "dtype must be CSC_F64 or CSC_F32");
-    // the local CSR is an ordinary num_rows x num_nodes CSR with global column indices
-    csc_graph* g = graph_create_impl(num_rows, num_nodes, nnz, indptr, indices, weights, dtype, device,
+    if (row_starts[0] != 0 || row_starts[nranks] != num_nodes) fail(CSC_ERR_INVALID, "row_starts must span [0, N]");
+    int64_t R = 0;
+    for (int q = 0; q < nranks; ++q) {
+      if (row_starts[q + 1] < row_starts[q]) fail(CSC_ERR_INVALID, "row_starts must be non-decreasing");
+      R = std::max<int64_t>(R, row_starts[q + 1] - row_starts[q]);
+    }
+    if (nnz > 0 && !indices) fail(CSC_ERR_INVALID, "indices is NULL");
+    const int64_t n = row_starts[rank + 1] - row_starts[rank];
+    // node id -> gather-panel row: rank q's rows occupy slots [q R, q R + rows_q) (monotone, so
+    // every row's columns stay sorted)
+    std::vector<int32_t> panel_idx((size_t)std::max<int64_t>(nnz, 1));
+    if ((int64_t)nranks * R >= (int64_t(1) << 31)) fail(CSC_ERR_INVALID, "gather panel rows exceed int32");
+    for (int64_t e = 0; e < nnz; ++e) {
+      const int64_t j = indices[e];
+      if (j < 0 || j >= num_nodes) fail(CSC_ERR_GRAPH, "column index out of range");
+      const int64_t q = std::upper_bound(row_starts, row_starts + nranks + 1, j) - row_starts - 1;
+      panel_idx[e] = (int32_t)(q * R + (j - row_starts[q]));
+    }
+    csc_graph* g = graph_create_impl(n, (int64_t)nranks * R, nnz, indptr, panel_idx.data(), weights, dtype, device,
                                      static_cast<cudaStream_t>(stream));
     g->n_global = num_nodes;
-    g->row_begin = row_begin;
+    g->row_begin = row_starts[rank];
+    g->shard_ranks = nranks;
+    g->shard_rank = rank;
+    g->shard_R = R;
+    g->gather_rows = (int64_t)nranks * R;
     *out = g;
   });
 }
@@ -480,35 +482,66 @@ int csc_graph_create_rows(int64_t num_nodes, int64_t row_begin, int64_t num_rows
 }  // extern "C"
 
 namespace {
-void filter_rows_entry(const csc_graph* g, csc_comm* comm, csc_peers* pe, const double* coeffs, int ncoeffs,
-                       const void* X, int64_t ldx, void* Y, int64_t ldy, int ncols, int io_dtype, int mode, double* out,
-                       void* stream) {
-  if (!g) fail(CSC_ERR_INVALID, "graph is NULL");
+// shards: one (NCCL / peers: this rank's) or all (group emulation) row shards of one graph
+void filter_rows_entry(const std::vector<const csc_graph*>& gs, csc_comm* comm, csc_peers* pe, const double* coeffs,
+                       int ncoeffs, const void* const* X, const int64_t* ldx, void* const* Y, const int64_t* ldy,
+                       int ncols, int io_dtype, int mode, double* const* out, void* stream) {
+  if (gs.empty() || !gs[0]) fail(CSC_ERR_INVALID, "graph is NULL");
   if (ncoeffs < 1 || !coeffs) fail(CSC_ERR_INVALID, "need coefficients");
   if (mode < 0 || mode > 2) fail(CSC_ERR_INVALID, "mode must be 0 (filter), 1 (sum of squares), 2 (row sums)");
-  if (ncols < 1 || ldx < ncols || (mode != 1 && (ldy < ncols || !Y))) fail(CSC_ERR_INVALID, "bad block");
-  if (mode != 0 && !out) fail(CSC_ERR_INVALID, "out is NULL");
-  const int dev = pe ? pe->device : comm->device;
-  if (dev != g->device) fail(CSC_ERR_INVALID, "transport and graph on different devices");
+  if (io_dtype != CSC_F64 && io_dtype != CSC_F32) fail(CSC_ERR_INVALID, "io_dtype must be CSC_F64 or CSC_F32");
+  const csc_graph* g0 = gs[0];
+  if (g0->shard_ranks < 1) fail(CSC_ERR_INVALID, "not a row shard (csc_graph_create_row_shard)");
+  const int nranks = pe ? pe->nranks : (comm ? comm->nranks : (int)gs.size());
+  if (g0->shard_ranks != nranks) fail(CSC_ERR_INVALID, "shard count and transport rank count differ");
+  if (!pe && !comm && (int)gs.size() != nranks) fail(CSC_ERR_INVALID, "group needs every shard");
+  const int my_rank = pe ? pe->rank : (comm ? comm->rank : -1);
+  for (size_t q = 0; q < gs.size(); ++q) {
+    const csc_graph* g = gs[q];
+    if (!g) fail(CSC_ERR_INVALID, "graph is NULL");
+    if (g->device != g0->device || g->dtype != g0->dtype || g->shard_ranks != nranks || g->shard_R != g0->shard_R ||
+        g->n_global != g0->n_global)
+      fail(CSC_ERR_INVALID, "shards of different graphs / devices / dtypes");
+    if (g->shard_rank != (my_rank >= 0 ? my_rank : (int)q)) fail(CSC_ERR_INVALID, "shard / rank mismatch");
+    // (a shard without rows may pass NULL blocks)
+    if (ncols < 1 || ldx[q] < ncols || (mode != 1 && (ldy[q] < ncols || (!Y[q] && g->n > 0))))
+      fail(CSC_ERR_INVALID, "bad block");
+    if (mode != 0 && !out[q]) fail(CSC_ERR_INVALID, "out is NULL");
+    if ((g->n > 0 && !is_device_ptr(X[q], g->device)) || (mode != 1 && g->n > 0 && !is_device_ptr(Y[q], g->device)))
+      fail(CSC_ERR_INVALID, "row-sharded blocks must be device buffers");
+  }
+  const int dev = g0->device;
+  if ((pe && pe->device != dev) || (comm && comm->device != dev))
+    fail(CSC_ERR_INVALID, "transport and graph on different devices");
   if (pe && !pe->ready) fail(CSC_ERR_INVALID, "peer transport not attached to every rank (csc_peers_attach)");
-  if (!is_device_ptr(X, g->device) || (mode != 1 && !is_device_ptr(Y, g->device)))
-    fail(CSC_ERR_INVALID, "row-sharded blocks must be device buffers");
-  DeviceGuard dg(g->device);
-  ensure_pool(g->device);
+  DeviceGuard dg(dev);
+  ensure_pool(dev);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  DeviceOut o(out, sizeof(double) * (mode == 2 ? g->n : 1), g->device, s);
-  double* dout = mode == 0 ? nullptr : o.as<double>();
-  if (g->dtype == CSC_F64 && io_dtype == CSC_F64)
-    run_rows<double, double>(g, comm, pe, coeffs, ncoeffs, (const double*)X, ldx, (double*)Y, ldy, ncols, mode, dout,
-                             s);
-  else if (g->dtype == CSC_F32 && io_dtype == CSC_F32)
-    run_rows<float, float>(g, comm, pe, coeffs, ncoeffs, (const float*)X, ldx, (float*)Y, ldy, ncols, mode, dout, s);
-  else if (g->dtype == CSC_F32 && io_dtype == CSC_F64)
-    run_rows<float, double>(g, comm, pe, coeffs, ncoeffs, (const double*)X, ldx, (double*)Y, ldy, ncols, mode, dout,
-                            s);
-  else
-    run_rows<double, float>(g, comm, pe, coeffs, ncoeffs, (const float*)X, ldx, (float*)Y, ldy, ncols, mode, dout, s);
-  if (mode != 0) o.finish();
+  std::vector<std::unique_ptr<DeviceOut>> os;
+  std::vector<double*> douts(gs.size(), nullptr);
+  for (size_t q = 0; q < gs.size(); ++q)
+    if (mode != 0) {
+      os.emplace_back(new DeviceOut(out[q], sizeof(double) * (mode == 2 ? std::max<int64_t>(gs[q]->n, 1) : 1), dev, s));
+      douts[q] = os.back()->as<double>();
+    }
+  std::vector<int64_t> lx(ldx, ldx + gs.size()), ly(gs.size(), 0);
+  for (size_t q = 0; q < gs.size(); ++q) ly[q] = mode == 1 ? 0 : ldy[q];
+  auto go = [&](auto tag_t, auto tag_io) {
+    using T = decltype(tag_t);
+    using Tio = decltype(tag_io);
+    std::vector<const Tio*> xs(gs.size());
+    std::vector<Tio*> ys(gs.size(), nullptr);
+    for (size_t q = 0; q < gs.size(); ++q) {
+      xs[q] = static_cast<const Tio*>(X[q]);
+      if (mode != 1) ys[q] = static_cast<Tio*>(Y[q]);
+    }
+    run_rows<T, Tio>(gs, comm, pe, coeffs, ncoeffs, xs, lx, ys, ly, ncols, mode, douts, s);
+  };
+  if (g0->dtype == CSC_F64 && io_dtype == CSC_F64) go(double(), double());
+  else if (g0->dtype == CSC_F32 && io_dtype == CSC_F32) go(float(), float());
+  else if (g0->dtype == CSC_F32) go(float(), double());
+  else go(double(), float());
+  for (auto& o : os) o->finish();
   CSC_CUDA(cudaStreamSynchronize(s));
 }
 }  // namespace
@@ -520,7 +553,7 @@ int csc_cheb_filter_rows(const csc_graph* g, csc_comm* comm, const double* coeff
                          void* stream) {
   return guard([&] {
     if (!comm) fail(CSC_ERR_INVALID, "comm is NULL");
-    filter_rows_entry(g, comm, nullptr, coeffs, ncoeffs, X, ldx, Y, ldy, ncols, io_dtype, mode, out, stream);
+    filter_rows_entry({g}, comm, nullptr, coeffs, ncoeffs, &X, &ldx, &Y, &ldy, ncols, io_dtype, mode, &out, stream);
   });
 }
 
@@ -529,7 +562,29 @@ int csc_cheb_filter_rows_peers(const csc_graph* g, csc_peers* peers, const doubl
                                double* out, void* stream) {
   return guard([&] {
     if (!peers) fail(CSC_ERR_INVALID, "peers is NULL");
-    filter_rows_entry(g, nullptr, peers, coeffs, ncoeffs, X, ldx, Y, ldy, ncols, io_dtype, mode, out, stream);
+    filter_rows_entry({g}, nullptr, peers, coeffs, ncoeffs, &X, &ldx, &Y, &ldy, ncols, io_dtype, mode, &out, stream);
+  });
+}
+
+int csc_cheb_filter_rows_group(const csc_graph* const* shards, int nshards, const double* coeffs, int ncoeffs,
+                               const void* const* X, const int64_t* ldx, void* const* Y, const int64_t* ldy, int ncols,
+                               int io_dtype, int mode, double* const* out, void* stream) {
+  return guard([&] {
+    if (!shards || nshards < 1 || !X || !ldx || (mode != 1 && (!Y || !ldy)) || (mode != 0 && !out))
+      fail(CSC_ERR_INVALID, "NULL argument");
+    std::vector<const csc_graph*> gs(shards, shards + nshards);
+    std::vector<void*> ys(nshards, nullptr);
+    std::vector<int64_t> lys(nshards, 0);
+    std::vector<double*> outs(nshards, nullptr);
+    for (int q = 0; q < nshards; ++q) {
+      if (mode != 1) {
+        ys[q] = Y[q];
+        lys[q] = ldy[q];
+      }
+      if (mode != 0) outs[q] = out[q];
+    }
+    filter_rows_entry(gs, nullptr, nullptr, coeffs, ncoeffs, X, ldx, ys.data(), lys.data(), ncols, io_dtype, mode,
+                      outs.data(), stream);
   });
 }
 

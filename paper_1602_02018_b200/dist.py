@@ -352,11 +352,38 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
 # is all-gathered over NCCL after every Chebyshev step (inside the library).
 
 
+def row_partition(indptr: np.ndarray, world: int) -> np.ndarray:
+    """Contiguous row ranges balanced by work ("balanced by nnz"):
+    ``starts`` (world + 1 entries) with rank q owning rows [starts[q], starts[q + 1]).
+
+    A step's per-rank cost is its CSR entries plus its dense rows, so the split balances
+    nnz + rows: cut where the cumulative count crosses q / world of the total."""
+    indptr = np.asarray(indptr, dtype=np.int64)
+    n = indptr.size - 1
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    cost = indptr + np.arange(n + 1, dtype=np.int64)  # cumulative nnz + rows at each row boundary
+    targets = cost[-1] * np.arange(1, world, dtype=np.float64) / world
+    cuts = np.searchsorted(cost, targets, side="left")
+    return np.concatenate([[0], np.minimum(cuts, n), [n]]).astype(np.int64)
+
+
 def row_range(num_nodes: int, world: int, rank: int) -> tuple[int, int]:
-    """Rows owned by ``rank``: R = ceil(N / world) consecutive rows (the last rank may own fewer)."""
+    """Equal-count split: R = ceil(N / world) consecutive rows (the last rank may own fewer)."""
     R = -(-num_nodes // world)
     begin = min(num_nodes, rank * R)
     return begin, min(num_nodes, begin + R)
+
+
+def _create_shard(graph, starts: np.ndarray, world: int, rank: int, dtype: str, device: int) -> tuple[int, int]:
+    begin, end = int(starts[rank]), int(starts[rank + 1])
+    indptr, indices, weights = local_csr(graph, begin, end)
+    h = C.c_void_p()
+    st = np.ascontiguousarray(starts, dtype=np.int64)
+    _lib.call("csc_graph_create_row_shard", graph.num_nodes, world, rank, _lib.ptr(st), int(indices.size),
+              _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(weights), _lib.dtype_code(dtype), device,
+              _lib.current_stream(device), C.byref(h))
+    return h.value, int(indices.size)
 
 
 def local_csr(graph, begin: int, end: int):
@@ -386,7 +413,7 @@ class RowShardedOperator:
     """
 
     def __init__(self, graph, grp: Group, dtype: str = "float32", device: int | None = None,
-                 transport: str = "nccl"):
+                 transport: str = "nccl", starts: np.ndarray | None = None):
         import torch
 
         if transport not in ("nccl", "peer"):
@@ -397,15 +424,12 @@ class RowShardedOperator:
         self.grp = grp
         self.num_nodes = graph.num_nodes
         self.device = _lib.default_device() if device is None else int(device)
-        self.begin, self.end = row_range(graph.num_nodes, grp.world, grp.rank)
+        self.starts = row_partition(graph.indptr, grp.world) if starts is None else np.asarray(starts, np.int64)
+        self.begin, self.end = int(self.starts[grp.rank]), int(self.starts[grp.rank + 1])
+        self.panel_R = int(np.diff(self.starts).max())
         self.dtype = dtype
-        indptr, indices, weights = local_csr(graph, self.begin, self.end)
-        h = C.c_void_p()
-        _lib.call("csc_graph_create_rows", graph.num_nodes, self.begin, self.end - self.begin, int(indices.size),
-                  _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(weights), _lib.dtype_code(dtype), self.device,
-                  _lib.current_stream(self.device), C.byref(h))
-        self.handle = h.value
-        self.local_nnz = int(indices.size)
+        self.handle, self.local_nnz = _create_shard(graph, self.starts, grp.world, grp.rank, dtype, self.device)
+        self.total_nnz = int(graph.indices.size)
         self.comm = None
         if transport == "peer":
             return
@@ -449,9 +473,9 @@ class RowShardedOperator:
     def _ensure_peers(self, ncols: int) -> None:
         """(Re)build the peer transport when this block needs wider panels (collective)."""
         row_bytes = C.c_int64(0)
-        _lib.call("csc_panel_row_bytes", self.num_nodes, ncols, _lib.dtype_code(self.dtype), self.device,
+        rows = self.panel_R * self.grp.world
+        _lib.call("csc_panel_row_bytes", rows, ncols, _lib.dtype_code(self.dtype), self.device,
                   self.local_nnz * self.grp.world, C.byref(row_bytes))
-        rows = -(-self.num_nodes // self.grp.world) * self.grp.world
         need = rows * int(row_bytes.value)
         if self.peers is not None and need <= self._peer_bytes:
             return
@@ -508,3 +532,71 @@ class RowShardedOperator:
         if getattr(self, "handle", None):
             lib.csc_graph_destroy(self.handle)
             self.handle = None
+
+
+class RowShardGroup:
+    """Every rank's row shard of one graph in this process, on one device: the multi-rank
+    row-sharded filter executed as ranks stepping in lockstep, the per-step all-gather done
+    as device copies (``csc_cheb_filter_rows_group``; same kernels, per-rank arguments and
+    panel layout as ``RowShardedOperator`` over NCCL).  Blocks are full N-row CUDA tensors;
+    shard q works on rows [starts[q], starts[q + 1]), a contiguous view."""
+
+    def __init__(self, graph, world: int, dtype: str = "float32", device: int | None = None,
+                 starts: np.ndarray | None = None):
+        self.num_nodes = graph.num_nodes
+        self.world = int(world)
+        self.device = _lib.default_device() if device is None else int(device)
+        self.dtype = dtype
+        self.starts = row_partition(graph.indptr, self.world) if starts is None else np.asarray(starts, np.int64)
+        self.handles, self.nnz = [], []
+        for q in range(self.world):
+            h, m = _create_shard(graph, self.starts, self.world, q, dtype, self.device)
+            self.handles.append(h)
+            self.nnz.append(m)
+
+    def _run(self, filt: PolyFilter, X, mode: int):
+        import torch
+
+        X = X.contiguous()
+        c = coeff_array(filt)
+        W = self.world
+        parts = [X[int(self.starts[q]): int(self.starts[q + 1])] for q in range(W)]
+        Y = torch.empty_like(X) if mode != 1 else None
+        yparts = [Y[int(self.starts[q]): int(self.starts[q + 1])] for q in range(W)] if Y is not None else None
+        outs = None
+        if mode == 1:
+            outs = torch.zeros((W,), dtype=torch.float64, device=X.device)
+            optr = [outs.data_ptr() + 8 * q for q in range(W)]
+        elif mode == 2:
+            outs = torch.zeros((X.shape[0],), dtype=torch.float64, device=X.device)
+            optr = [outs.data_ptr() + 8 * int(self.starts[q]) for q in range(W)]
+        arr = lambda vals, t=C.c_void_p: (t * W)(*vals)  # noqa: E731
+        ld = [int(X.stride(0))] * W
+        _lib.call("csc_cheb_filter_rows_group", arr(self.handles), W, _lib.ptr(c), int(c.size),
+                  arr([p.data_ptr() for p in parts]), arr(ld, C.c_int64),
+                  None if Y is None else arr([p.data_ptr() for p in yparts]),
+                  None if Y is None else arr(ld, C.c_int64), int(X.shape[1]), _lib.dtype_code(X.dtype), mode,
+                  None if outs is None else arr(optr), _lib.current_stream(self.device))
+        return Y, outs
+
+    def apply_filter(self, filt: PolyFilter, X):
+        return self._run(filt, X, 0)[0]
+
+    def eigencount(self, filt: PolyFilter, R) -> float:
+        """Per-rank partial sums of squares, summed in rank order (as RowShardedOperator)."""
+        _, part = self._run(filt, R, 1)
+        total = 0.0
+        for v in part.cpu().numpy().tolist():
+            total += v
+        return float(total)
+
+    def filter_rowsq(self, filt: PolyFilter, R):
+        return self._run(filt, R, 2)
+
+    def __del__(self):
+        lib = _lib._lib
+        if lib is None:
+            return
+        for h in getattr(self, "handles", []):
+            lib.csc_graph_destroy(h)
+        self.handles = []

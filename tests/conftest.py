@@ -13,6 +13,10 @@ if str(ROOT) not in sys.path:
 
 GOLDEN = ROOT / "tests" / "golden"
 
+# the reference's own test modules run through tests/ref_suite/run.py (own rootdir and a
+# ``cscluster`` alias), driven by tests/test_gpu_ref_suite.py, never collected directly
+collect_ignore = ["ref_suite"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libcsc_b200.so")

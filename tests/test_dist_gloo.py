@@ -171,15 +171,37 @@ def test_row_range_partitions():
             assert max(b - a for a, b in ranges) == -(-N // world)
 
 
+def test_row_partition_balances_nnz():
+    """row_partition cuts contiguous ranges whose nnz + rows cost is within one row of the
+    ideal share, also on heavy-tailed DC-SBM rows."""
+    from paper_1602_02018_b200.sbm import SbmConfig, critical_epsilon, dcsbm_edges
+
+    cfg = SbmConfig(num_nodes=20000, k=20, avg_degree=5.5, epsilon=critical_epsilon(5.5, 20) / 4.0, seed=0)
+    src, dst, _, _ = dcsbm_edges(cfg)
+    deg = np.bincount(np.concatenate([src, dst]), minlength=cfg.num_nodes)
+    indptr = np.concatenate([[0], np.cumsum(deg)])
+    row_cost = deg + 1
+    for world in (1, 2, 3, 8, 64):
+        st = D.row_partition(indptr, world)
+        assert st[0] == 0 and st[-1] == cfg.num_nodes and np.all(np.diff(st) >= 0) and st.size == world + 1
+        costs = [int(row_cost[st[q]:st[q + 1]].sum()) for q in range(world)]
+        assert max(costs) <= row_cost.sum() / world + row_cost.max()
+    # equal-cost rows reduce to the equal-count split
+    flat = np.arange(0, 16 * 1001, 16)
+    assert D.row_partition(flat, 4).tolist() == [0, 250, 500, 750, 1000]
+
+
 def _row_sharded_filter(grp):
     """The row-sharded recurrence of rows.cu, restated with numpy: local rows x full block,
-    block all-gathered after every step (equal R-row chunks, padded)."""
+    nnz-balanced row ranges (row_partition), block all-gathered after every step in equal
+    R = max-rows slots (padded), read back through the slot layout."""
     import scipy.sparse as sp
 
     csr = c1_csr()
     N = csr.num_nodes
-    b, e = D.row_range(N, grp.world, grp.rank)
-    R = -(-N // grp.world)
+    starts = D.row_partition(csr.indptr, grp.world)
+    b, e = int(starts[grp.rank]), int(starts[grp.rank + 1])
+    R = int(np.diff(starts).max())
     indptr, indices, weights = D.local_csr(csr, b, e)
     Wl = sp.csr_matrix((weights, indices, indptr), shape=(e - b, N))
     dis = csr.dis
@@ -189,7 +211,8 @@ def _row_sharded_filter(grp):
     def gather(local):
         pad = np.zeros((R, local.shape[1]))
         pad[: local.shape[0]] = local
-        return np.concatenate(grp.all_gather(pad), axis=0)[:N]
+        slots = grp.all_gather(pad)
+        return np.concatenate([slots[q][: starts[q + 1] - starts[q]] for q in range(grp.world)], axis=0)
 
     def A(full, rows):  # (L - I) restricted to this rank's rows: -D^-1/2 W D^-1/2
         return -(dis[b:e, None] * (Wl @ (dis[:, None] * full)))

@@ -291,3 +291,26 @@ def test_bench_reference_arm_contract_on_cpu():
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] in ("port", "reference")
+    assert line["scaling"] == "strong" and line["n_gpus"] == 1
+
+
+def test_bench_self_launches_ranks_for_gpus_n():
+    """bench.py --gpus 2 without WORLD_SIZE re-launches itself under torch.distributed.run: two
+    ranks start, rank 0 alone prints the line (reference arm: CPU-only, so it runs here)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=300, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference"
+    assert "2 rank(s)" in line["config"]["parallelism"]
