@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
   // size): fewer registers in the neighbour loop
   const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  const uint32_t SV = (uint32_t)a.sv;  // row stride in vectors (<= LPR; == LPR unless the panel is tight)
   const V* __restrict__ Gv = static_cast<const V*>(a.G) + sub;
 
   const T* __restrict__ G = static_cast<const T*>(a.G);
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
     const bool rok = row < n;
     const bool on = rok && lane_on;
     const int cnt = nend - nbeg;
-    const uint32_t voff = (uint32_t)row * LPR + sub;  // this lane's vector in row-local streams
+    const uint32_t voff = (uint32_t)row * SV + sub;  // this lane's vector in row-local streams
     const size_t off = (size_t)voff * VEC;
 
     // 1. row-local operands: loaded after the neighbour loop (latency hidden by
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
           gv[k] = VT::zero();
-          if (jc[k] >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)jc[k] * LPR);
+          if (jc[k] >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)jc[k] * SV);
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
       }
       if constexpr (EPI == EPI_NONE) {  // (peer stores happen on mid steps only)
       if (a.npeers > 0) {  // fused all-gather: this row into every rank's next gather panel
-        const size_t poff = (size_t)(a.peer_row0 + row) * PW + col0;
+        const size_t poff = (size_t)(a.peer_row0 + row) * (SV * VEC) + col0;
         for (int q = 0; q < a.npeers; ++q)
           *reinterpret_cast<V*>(static_cast<T*>(a.peers[q]) + poff) = VT::make(out);
       }
@@ -345,10 +346,11 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
       for (int c = 0; c < VEC; ++c) red[threadIdx.x >> 5][col0 + c] = cd[c];
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < PW; t += blockDim.x) {
+    const int pwr = (int)SV * VEC;  // the partials' row stride is the panel width
+    for (int t = threadIdx.x; t < pwr; t += blockDim.x) {
       double sum = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += red[w][t];
-      a.part[(size_t)blockIdx.x * PW + t] = sum;
+      a.part[(size_t)blockIdx.x * pwr + t] = sum;
     }
   }
 }
@@ -377,6 +379,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
   const int n = (int)a.n;
   const int ngroups = (n + GPW - 1) / GPW;
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  const uint32_t SV = (uint32_t)a.sv;  // row stride in vectors (<= LPR)
   const V* __restrict__ Gv = static_cast<const V*>(a.G) + sub;
   const T ka = static_cast<T>(a.ka), ks = static_cast<T>(a.ks), kx = static_cast<T>(a.kx);
   int gi = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
           const int32_t j = LPR == 1 ? jj[k] : __shfl_sync(FULL, jj[k / LPR], k % LPR, LPR);
           if constexpr (!UNIT) wk[k] = LPR == 1 ? ww[k] : __shfl_sync(FULL, ww[k / LPR], k % LPR, LPR);
           gv[k] = VT::zero();
-          if (j >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)j * LPR);
+          if (j >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)j * SV);
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
       }
     }
     if (row < n && lane_on) {
-      const uint32_t off = ((uint32_t)row * LPR + sub) * VEC;
+      const uint32_t off = ((uint32_t)row * SV + sub) * VEC;
       const T si = static_cast<const V2*>(a.rs)[row].x;
       const T kacc = ka * (si * si);  // as k_cheb_step (bit-identical results)
       T out[VEC], sv[VEC], xv[VEC];
@@ -603,7 +606,10 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   a.hints = g_opt.cache_hints.load() != 0;
   a.contig = g_opt.row_order.load() == 1;
   constexpr int VEC = 16 / sizeof(T);
-  const int lpr = pw / VEC;
+  if (pw < VEC || pw % VEC != 0 || pw > 32 * VEC) fail(CSC_ERR_INVALID, "unsupported panel width");
+  a.sv = pw / VEC;
+  int lpr = 1;  // lanes per row: the power of two >= the row's vectors
+  while (lpr < a.sv) lpr *= 2;
   // rows of the gathered panel: the local rows, or every rank's slots of a row shard
   const int64_t gsrc = std::max<int64_t>(a.n, g->gather_rows);
   if (gsrc > 0 && (uint64_t)gsrc * (uint64_t)lpr >= (1ull << 32))
@@ -624,7 +630,7 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
                     a.npeers == 0 && a.G != nullptr && a.O != nullptr && !a.contig && threads == 256 &&
                     g_opt.unroll.load() == 4 && g_opt.persistent.load() && persist_bytes(g->device) == 0 &&
                     lpr != 2 &&
-                    (double)gsrc * lpr * 16.0 <= 4.0 * (double)device_props(g->device).l2_bytes;
+                    (double)gsrc * a.sv * 16.0 <= 4.0 * (double)device_props(g->device).l2_bytes;
   if (lean) {
     switch (lpr) {
       case 1: grid = launch_mid<T, 1>(a, g->device, s); break;
@@ -829,7 +835,7 @@ template int filter_panel<double>(const csc_graph*, const double*, int, const do
 
 // ---------------------------------------------------------------------------
 // panels
-PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
+PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz, bool tight) {
   const int vec = 16 / (int)dtype_size(dtype);
   const int max_lpr = 32;
   int max_pw = vec * max_lpr;
@@ -868,6 +874,8 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
     int pw;
     if (rem >= max_pw) {
       pw = max_pw;
+    } else if (tight) {
+      pw = (rem + vec - 1) / vec * vec;
     } else {
       pw = vec;
       while (pw < rem) pw *= 2;
@@ -1014,12 +1022,12 @@ __global__ void k_normalize_rows(const T* __restrict__ Yp, const double* __restr
 // panel): LPR lanes per row move 16-byte vectors, several rows per warp, stores vectorised;
 // same arithmetic as k_normalize_rows (fp64 v / ||row||, features.py:84-87).
 template <typename T, typename To, int LPR>
-__global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, int wc, const double* __restrict__ rowsq,
+__global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, int pw, int wc,
+                                                      const double* __restrict__ rowsq,
                                                       int64_t n, To* __restrict__ F, int64_t ldf,
                                                       uint8_t* __restrict__ zflag,
                                                       unsigned long long* __restrict__ nzero) {
   constexpr int VEC = 16 / (int)sizeof(T);
-  constexpr int PW = LPR * VEC;
   constexpr int GPW = 32 / LPR;
   const int lane = threadIdx.x & 31, sub = lane % LPR, grp = lane / LPR;
   const int col0 = sub * VEC;
@@ -1031,10 +1039,10 @@ __global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, 
       T v[VEC];
       if (col0 < wc) {
         if constexpr (sizeof(T) == 4) {
-          const float4 q = __ldcs(reinterpret_cast<const float4*>(Yp + row * PW + col0));
+          const float4 q = __ldcs(reinterpret_cast<const float4*>(Yp + row * pw + col0));
           v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
         } else {
-          const double2 q = __ldcs(reinterpret_cast<const double2*>(Yp + row * PW + col0));
+          const double2 q = __ldcs(reinterpret_cast<const double2*>(Yp + row * pw + col0));
           v[0] = q.x, v[1] = q.y;
         }
       }
@@ -1076,14 +1084,15 @@ static bool launch_normalize_1p(const PanelPlan& pp, const T* Yp, const double* 
   constexpr int VEC = 16 / (int)sizeof(T);
   if (pp.np != 1 || ((size_t)ldf * sizeof(To)) % 16 != 0 || reinterpret_cast<uintptr_t>(F) % 16 != 0) return false;
   if ((VEC * sizeof(To)) % 16 != 0 && VEC * sizeof(To) != 8) return false;
-  const int lpr = pp.pw[0] / VEC;
+  int lpr = 1;
+  while (lpr < pp.pw[0] / VEC) lpr *= 2;
   const int64_t rows_per_block = 8 * (32 / lpr);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + rows_per_block - 1) / rows_per_block,
                                                                (int64_t)device_props(device).sms * 8));
   switch (lpr) {
 #define CSC_NORM1P(L)                                                                                        \
   case L:                                                                                                    \
-    k_normalize_1p<T, To, L><<<grid, 256, 0, s>>>(Yp, pp.wc[0], rowsq, n, F, ldf, zflag, nzero);             \
+    k_normalize_1p<T, To, L><<<grid, 256, 0, s>>>(Yp, pp.pw[0], pp.wc[0], rowsq, n, F, ldf, zflag, nzero);  \
     break;
     CSC_NORM1P(1)
     CSC_NORM1P(2)
@@ -1201,7 +1210,7 @@ struct PackedInput {
   PanelPlan pp;
   Scratch x, xs;
   PackedInput(const csc_graph* g, const void* src, int64_t ld, int ncols, int io, cudaStream_t s) {
-    pp = plan_panels(g->n, ncols, g->dtype, g->device, g->nnz);
+    pp = plan_panels(g->n, ncols, g->dtype, g->device, g->nnz, g_opt.tight_panels.load() != 0);
     const size_t cs = dtype_size(g->dtype);
     StagedIn in;
     stage_in(src, ld, g->n, ncols, io, g->device, s, in);

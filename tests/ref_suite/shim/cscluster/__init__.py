@@ -17,6 +17,7 @@ import at module level are supplied here as test doubles or stubs:
 
 from __future__ import annotations
 
+import importlib
 import sys
 from dataclasses import dataclass
 
@@ -24,9 +25,6 @@ import numpy as np
 
 import paper_1602_02018_b200 as _P
 from paper_1602_02018_b200 import *  # noqa: F401,F403
-from paper_1602_02018_b200 import (  # noqa: F401
-    features, filters, graph, kmeans as _kmeans_mod, pipeline, result, sampling, sbm, spectrum, _rng,
-)
 
 DEFAULT_DENSE_CAP = 5000
 
@@ -75,8 +73,7 @@ _oracle = type(sys)("cscluster.oracle")
 _oracle.EigenBasis, _oracle.dense_eig, _oracle.DenseCapError = EigenBasis, dense_eig, DenseCapError
 _oracle.DEFAULT_DENSE_CAP = DEFAULT_DENSE_CAP
 
-for _mod, _obj in (("graph", graph), ("filters", filters), ("spectrum", spectrum), ("features", features),
-                   ("sampling", sampling), ("pipeline", pipeline), ("kmeans", _kmeans_mod), ("result", result),
-                   ("sbm", sbm), ("_rng", _rng), ("oracle", _oracle)):
-    sys.modules[f"cscluster.{_mod}"] = _obj
-kmeans = _P.kmeans  # the function (the submodule alias above must not shadow it)
+# submodules by import path: the package attribute ``kmeans`` is the function, not the module
+for _mod in ("graph", "filters", "spectrum", "features", "sampling", "pipeline", "kmeans", "result", "sbm", "_rng"):
+    sys.modules[f"cscluster.{_mod}"] = importlib.import_module(f"paper_1602_02018_b200.{_mod}")
+sys.modules["cscluster.oracle"] = _oracle
