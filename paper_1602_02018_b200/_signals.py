@@ -118,7 +118,14 @@ def device_normal_block(rng: np.random.Generator, n: int, w: int, device: int = 
     _lib.call("csc_numpy_normals", C.c_uint64(state >> 64), C.c_uint64(state & ((1 << 64) - 1)),
               C.c_uint64(inc >> 64), C.c_uint64(inc & ((1 << 64) - 1)), int(n) * int(w), divisor, out.data_ptr(),
               C.byref(consumed), int(device), stream.cuda_stream if stream is not None else _lib.current_stream(device))
+    # advance() also clears PCG64's buffered 32-bit half; the host standard_normal draw
+    # leaves it alone, so carry it over
+    buffered = rng.bit_generator.state
     rng.bit_generator.advance(int(consumed.value))
+    if buffered["has_uint32"]:
+        st = rng.bit_generator.state
+        st["has_uint32"], st["uinteger"] = buffered["has_uint32"], buffered["uinteger"]
+        rng.bit_generator.state = st
     return out
 
 

@@ -115,6 +115,7 @@ class DeviceBackend:
     """Per-rank compute on the rank's GPU through the C ABI (host numpy in/out, device-resident blocks)."""
 
     def __init__(self, op):
+        self.num_edges = op.graph.num_edges
         import torch
 
         self.op = op
@@ -255,6 +256,8 @@ def _normal_columns(backend, rng, n: int, w: int, cols: slice):
 def estimate_lambda_k_sharded(backend, N: int, k: int, order: int, ds: int | None, rng, grp: Group,
                               max_steps: int = 20, refine: bool = False):
     """Dichotomy of spectrum.py:90-140 with the probe columns sharded over ranks."""
+    if not 1 <= k < N:
+        raise ValueError(f"k={k} out of range for N={N}")
     ds = ds if ds is not None else default_num_signals(N)
     cols = column_slice(ds, grp.world, grp.rank)
     lo, hi = 0.0, 2.0
@@ -299,17 +302,24 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
         if warn:
             warnings.append("lambda_k bracket fallback")
     timings["probe"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     low = design_lowpass(lam, prm.p, damping=prm.damping)
     high = matched_highpass(low)
+    timings["design"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     dcols = column_slice(prm.d, grp.world, grp.rank)
-    F, zero_rows = sharded_features(backend, low, _normal_columns(backend, substream(prm.seed, "signals"), N,
-                                                                  prm.d, dcols), grp)
+    R = _normal_columns(backend, substream(prm.seed, "signals"), N, prm.d, dcols)
+    timings["signals"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    F, zero_rows = sharded_features(backend, low, R, grp)
+    del R
     if zero_rows.size:
         warnings.append(f"{zero_rows.size} zero-norm feature rows")
     timings["filter"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     sampling = draw_sampling(N, prm.n, substream(prm.seed, "sampling"), exclude=zero_rows)
+    timings["sampling"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     # ranks own different numbers of feature columns when d % world != 0: exchange the
     # sampled rows column-major so the variable extent is the leading axis
     part = np.ascontiguousarray(np.asarray(backend.gather(F, sampling.indices)).T)
@@ -335,14 +345,16 @@ def run_csc_sharded(backend, num_nodes: int, params, grp: Group) -> ClusterResul
     if not bool(np.all(conv)):
         warnings.append("interpolation solver did not reach tolerance")
     diagnostics = {
-        "method": "csc", "num_nodes": N, "k": prm.k, "n": prm.n, "d": prm.d, "p": prm.p, "gamma": prm.gamma,
+        "method": "csc", "num_nodes": N, "num_edges": getattr(backend, "num_edges", None), "k": prm.k, "n": prm.n, "d": prm.d, "p": prm.p, "gamma": prm.gamma,
         "seed": prm.seed, "lambda_k_hat": lam, "lambda_source": source, "lambda_warning": warn,
         "probe_iterations": len(trace), "kmeans_inertia": labeling.inertia,
         "kmeans_iterations": labeling.iterations_run, "solver_iterations": its.tolist(),
         "solver_residuals": res.tolist(), "solver_converged": conv.tolist(), "ridge": icfg.ridge,
         "zero_feature_rows": zero_rows.tolist(), "assign_fallback_nodes": fallback.tolist(), "warnings": warnings,
-        "ranks": grp.world, "columns_per_rank": {"d": dcols.stop - dcols.start, "k": kcols.stop - kcols.start},
         "timings": {**timings, "total": time.perf_counter() - t_run},
+        # the only key a single-process run_csc does not write: this rank's share of the columns
+        "sharding": {"ranks": grp.world, "rank": grp.rank,
+                     "columns_per_rank": {"d": dcols.stop - dcols.start, "k": kcols.stop - kcols.start}},
     }
     return ClusterResult(labels=labels, soft=X, diagnostics=diagnostics, num_clusters=prm.k)
 

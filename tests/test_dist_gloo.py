@@ -9,6 +9,8 @@ from __future__ import annotations
 import os
 import socket
 
+import json
+
 import numpy as np
 import pytest
 import torch.distributed as dist
@@ -28,6 +30,8 @@ class OracleBackend:
 
     def __init__(self, csr):
         self.csr = csr
+        rows = np.repeat(np.arange(csr.num_nodes), np.diff(csr.indptr))
+        self.num_edges = int(np.count_nonzero(np.asarray(csr.indices) > rows))  # Graph.num_edges: i < j entries
 
     def count(self, filt, R):
         if R.shape[1] == 0:
@@ -144,18 +148,26 @@ def test_sharded_features_and_count_match_single_process():
 def _run_sharded(grp):
     be = OracleBackend(c1_csr())
     res = D.run_csc_sharded(be, 1000, CscParams(k=20, d=D_C1, seed=0), grp)
-    return res.labels, res.diagnostics["lambda_k_hat"], res.diagnostics["solver_iterations"], res.num_clusters
+    return res.labels, res.diagnostics["lambda_k_hat"], res.diagnostics["solver_iterations"], res.num_clusters, \
+        res.diagnostics
 
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_run_csc_sharded_matches_reference(c1_golden, world):
     # world 3: uneven column slices (d = 28, k = 20, ds = 14 do not divide by 3)
+    ref = json.loads(bytes(c1_golden["result_json"]).decode())["diagnostics"]
     parts = run_world(_run_sharded, world=world)
-    for labels, lam, its, k in parts:
+    for labels, lam, its, k, diag in parts:
         assert lam == float(c1_golden["lambda_k_hat"])
         assert its == c1_golden["solver_iterations"].tolist()
         assert np.array_equal(labels, c1_golden["labels"])
         assert k == 20
+        # same diagnostics schema as the reference (to_json drops timings), plus one nested key
+        assert set(diag) - {"timings", "sharding"} == set(ref)
+        assert set(diag["timings"]) == {"probe", "design", "signals", "filter", "sampling", "kmeans", "interpolate",
+                                        "total"}
+        assert diag["num_edges"] == ref["num_edges"]
+        assert diag["sharding"]["ranks"] == world
 
 
 # ---- row sharding (BASELINE config 5) -----------------------------------------

@@ -23,6 +23,18 @@ def test_device_normals_bit_exact(n, w):
         assert a.standard_normal() == b.standard_normal()
 
 
+def test_device_normals_keep_buffered_uint32():
+    """A generator holding a pending 32-bit half (after a 32-bit integers draw) keeps it."""
+    a, b = np.random.default_rng(5), np.random.default_rng(5)
+    a.integers(0, 1000, dtype=np.uint32)
+    b.integers(0, 1000, dtype=np.uint32)
+    assert a.bit_generator.state["has_uint32"] == 1
+    got = device_normal_block(a, 1000, 3).cpu().numpy()
+    assert np.array_equal(got, b.standard_normal((1000, 3)) / np.sqrt(3))
+    assert a.bit_generator.state == b.bit_generator.state
+    assert a.integers(0, 1000, 5, dtype=np.uint32).tolist() == b.integers(0, 1000, 5, dtype=np.uint32).tolist()
+
+
 def test_device_normals_continue_the_stream():
     """Consecutive blocks (the dichotomy's probes) match consecutive numpy draws."""
     a, b = substream(0, "probe"), substream(0, "probe")
