@@ -177,11 +177,12 @@ class NormalStream:
 
 
 def pcg_state(rng: np.random.Generator) -> tuple[int, int]:
+    """128-bit state and increment of a PCG64 generator.  A buffered 32-bit half
+    (``has_uint32``) is not part of the 64-bit stream the double draws consume; callers that
+    advance the generator carry it over (``_signals.device_normal_block``)."""
     st = rng.bit_generator.state
     if st["bit_generator"] != "PCG64":
         raise ValueError("parity RNG needs a PCG64 generator")
-    if st.get("has_uint32"):
-        raise ValueError("generator holds a buffered uint32; draw order would diverge")
     return int(st["state"]["state"]), int(st["state"]["inc"])
 
 

@@ -76,4 +76,9 @@ _oracle.DEFAULT_DENSE_CAP = DEFAULT_DENSE_CAP
 # submodules by import path: the package attribute ``kmeans`` is the function, not the module
 for _mod in ("graph", "filters", "spectrum", "features", "sampling", "pipeline", "kmeans", "result", "sbm", "_rng"):
     sys.modules[f"cscluster.{_mod}"] = importlib.import_module(f"paper_1602_02018_b200.{_mod}")
+    # and as package attributes, where no public name shadows them (monkeypatch resolves
+    # "cscluster.pipeline.kmeans" by getattr from the package)
+    if _mod not in globals():
+        globals()[_mod] = sys.modules[f"cscluster.{_mod}"]
 sys.modules["cscluster.oracle"] = _oracle
+oracle = _oracle
