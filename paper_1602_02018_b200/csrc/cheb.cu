@@ -863,6 +863,14 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz, bool
       int one = vec;
       while (one < w) one *= 2;
       pw = std::max(pw, one);
+      // ... unless that one panel's gather source spills L2 while 128-B-row panels fit it
+      // (fp32): C3 d = 56 as 2 x 32 columns, 24.55 -> 23.89 ms per filter, the inter-community
+      // gathers then hit L2; fp64 (256-B rows: 44.3 -> 49.4 ms) and L2-resident blocks (C4:
+      // 6.04 -> 7.64 ms) keep one panel (profiles/r02_ab_two_panels.txt)
+      const double l2 = (double)device_props(device).l2_bytes;
+      const int p128 = 128 / (int)dtype_size(dtype);
+      if (dtype == CSC_F32 && pw > p128 && (double)n * pw * dtype_size(dtype) > l2 && (double)n * 128.0 <= l2)
+        pw = p128;
     }
     max_pw = std::min(pw, max_pw);
   }
@@ -1021,8 +1029,11 @@ __global__ void k_normalize_rows(const T* __restrict__ Yp, const double* __restr
 // Single-panel features (the whole block in one panel, e.g. C3's d = 56 in one 64-wide
 // panel): LPR lanes per row move 16-byte vectors, several rows per warp, stores vectorised;
 // same arithmetic as k_normalize_rows (fp64 v / ||row||, features.py:84-87).
+// Also multi-panel blocks whose panels share one width (C3's d = 56 as 2 x 32 columns): panel
+// j's rows follow panel j-1's, its columns start at j * pw, and a row's norm sums the panels'
+// partial squares in panel order, as k_normalize_rows does.
 template <typename T, typename To, int LPR>
-__global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, int pw, int wc,
+__global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, int pw, int np, int ncols,
                                                       const double* __restrict__ rowsq,
                                                       int64_t n, To* __restrict__ F, int64_t ldf,
                                                       uint8_t* __restrict__ zflag,
@@ -1036,23 +1047,28 @@ __global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, 
   unsigned zeros = 0;
   for (int64_t row = warp * GPW + grp; row - grp < n; row += nw * GPW) {
     if (row < n) {
+      double t = rowsq[row];
+      for (int j = 1; j < np; ++j) t += rowsq[(int64_t)j * n + row];
+      const double nrm = sqrt(t);
+      const bool zero = nrm <= 1e-300;  // features.py:23, 81
+      for (int j = 0; j < np; ++j) {
+      const int wc = min(pw, ncols - j * pw);
       T v[VEC];
       if (col0 < wc) {
+        const T* src = Yp + ((int64_t)j * n + row) * pw + col0;
         if constexpr (sizeof(T) == 4) {
-          const float4 q = __ldcs(reinterpret_cast<const float4*>(Yp + row * pw + col0));
+          const float4 q = __ldcs(reinterpret_cast<const float4*>(src));
           v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
         } else {
-          const double2 q = __ldcs(reinterpret_cast<const double2*>(Yp + row * pw + col0));
+          const double2 q = __ldcs(reinterpret_cast<const double2*>(src));
           v[0] = q.x, v[1] = q.y;
         }
       }
-      const double nrm = sqrt(rowsq[row]);
-      const bool zero = nrm <= 1e-300;  // features.py:23, 81
       if (col0 < wc) {
         To o[VEC];
 #pragma unroll
         for (int c = 0; c < VEC; ++c) o[c] = zero ? To(0) : static_cast<To>((double)v[c] / nrm);
-        To* dst = F + row * ldf + col0;
+        To* dst = F + row * ldf + j * pw + col0;
         if (col0 + VEC <= wc) {  // 16-B aligned: ldf * sizeof(To) and col0 * sizeof(To) are multiples of 16
           if constexpr (sizeof(To) == 4 && VEC == 4) {
             __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
@@ -1069,6 +1085,7 @@ __global__ void __launch_bounds__(256) k_normalize_1p(const T* __restrict__ Yp, 
           for (int c = 0; c < wc - col0; ++c) dst[c] = o[c];
         }
       }
+      }
       if (sub == 0) {
         if (zflag) zflag[row] = zero ? 1 : 0;
         zeros += zero ? 1u : 0u;
@@ -1082,7 +1099,13 @@ template <typename T, typename To>
 static bool launch_normalize_1p(const PanelPlan& pp, const T* Yp, const double* rowsq, int64_t n, To* F, int64_t ldf,
                                 uint8_t* zflag, unsigned long long* nzero, int device, cudaStream_t s) {
   constexpr int VEC = 16 / (int)sizeof(T);
-  if (pp.np != 1 || ((size_t)ldf * sizeof(To)) % 16 != 0 || reinterpret_cast<uintptr_t>(F) % 16 != 0) return false;
+  if (((size_t)ldf * sizeof(To)) % 16 != 0 || reinterpret_cast<uintptr_t>(F) % 16 != 0) return false;
+  int ncols = 0;
+  for (int j = 0; j < pp.np; ++j) {  // equal-width panels, back to back (every panel but the last full)
+    if (pp.pw[j] != pp.pw[0] || pp.off[j] != (int64_t)j * n * pp.pw[0] || pp.c0[j] != j * pp.pw[0]) return false;
+    if (j + 1 < pp.np && pp.wc[j] != pp.pw[j]) return false;
+    ncols += pp.wc[j];
+  }
   if ((VEC * sizeof(To)) % 16 != 0 && VEC * sizeof(To) != 8) return false;
   int lpr = 1;
   while (lpr < pp.pw[0] / VEC) lpr *= 2;
@@ -1092,7 +1115,7 @@ static bool launch_normalize_1p(const PanelPlan& pp, const T* Yp, const double* 
   switch (lpr) {
 #define CSC_NORM1P(L)                                                                                        \
   case L:                                                                                                    \
-    k_normalize_1p<T, To, L><<<grid, 256, 0, s>>>(Yp, pp.pw[0], pp.wc[0], rowsq, n, F, ldf, zflag, nzero);  \
+    k_normalize_1p<T, To, L><<<grid, 256, 0, s>>>(Yp, pp.pw[0], pp.np, ncols, rowsq, n, F, ldf, zflag, nzero); \
     break;
     CSC_NORM1P(1)
     CSC_NORM1P(2)

@@ -265,7 +265,7 @@ def test_block_cg_column_compaction_is_exact(c1_golden, dtype, tol):
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_fast_single_panel_normalisation_bit_identical(c1_golden, dtype):
-    """The vectorised single-panel normaliser (default) and the general one give the same bytes,
+    """The vectorised single-/equal-width-panel normaliser (default) and the general one give the same bytes,
     zero rows and flags included (isolated nodes whose signal rows are zero), for host fp64 and
     device outputs of the compute dtype, at widths that fill a panel exactly and partially."""
     import torch
@@ -276,12 +276,16 @@ def test_fast_single_panel_normalisation_bit_identical(c1_golden, dtype):
     op = P.laplacian_op(gi, dtype=dtype)
     low = P.design_lowpass(0.4, 30)
     rng = np.random.default_rng(9)
-    for w in (3, 16, 28, 31, 64 if dtype == "float32" else 32):
+    # panel_width forced narrow: multi-panel blocks (equal-width panels take the vectorised
+    # normaliser too, e.g. w = 31 as 4 x 8 fp32 columns; w = 28 ends in a narrower panel)
+    narrow = 8 if dtype == "float32" else 4
+    for w, pwopt in [(3, 0), (16, 0), (28, 0), (31, 0), (64 if dtype == "float32" else 32, 0), (28, narrow),
+                     (31, narrow), (2 * narrow, narrow)]:
         X = rng.standard_normal((gi.num_nodes, w))
         X[-5:-2] = 0.0
         out = {}
         for fast in (0, 1):
-            with options(fast_normalize=fast):
+            with options(fast_normalize=fast, panel_width=pwopt):
                 F = np.empty_like(X)
                 z = P.features.features_into(op, low, X, F)
                 Xd = torch.tensor(X, device="cuda", dtype=torch.float32 if dtype == "float32" else torch.float64)
