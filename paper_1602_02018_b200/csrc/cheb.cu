@@ -284,8 +284,9 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
       }
       if (a.fwd && Y != nullptr) st_stream(HINTS, reinterpret_cast<V*>(Y + off), VT::make(res));
       if (O != nullptr) {
-        // default write-back: this panel is the next step's gather source, let it stay in L2
-        *reinterpret_cast<V*>(O + off) = VT::make(out);
+        // this panel is the next step's gather source; evict-first unless option l2_policy = 0
+        // (it would push this step's gather source out of L2; measured in k_cheb_mid)
+        st_stream(a.pol != 0, reinterpret_cast<V*>(O + off), VT::make(out));
       }
       if constexpr (EPI == EPI_NONE) {  // (peer stores happen on mid steps only)
       if (a.npeers > 0) {  // fused all-gather: this row into every rank's next gather panel
@@ -362,7 +363,9 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 // Same schedule and chunking as k_cheb_step, with only the state that case needs, so it
 // fits 32 registers and runs 64 warps per SM (8 CTAs of 256 threads); 256-B rows use the
 // 40-register / 6-CTA build (five gathers in flight per lane).
-template <typename T, int LPR, int MINB, bool UNIT>
+// OUT_EF: the output panel (the next step's gather source) is stored evict-first, so it does not
+// push this step's gather source out of an L2 it barely fits (option l2_policy)
+template <typename T, int LPR, int MINB, bool UNIT, bool OUT_EF = false>
 __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
   using VT = Vec16<T>;
   using V = typename VT::type;
@@ -466,7 +469,11 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
       if (a.X && a.kx != 0.0) VT::unpack(__ldcs(reinterpret_cast<const V*>(static_cast<const T*>(a.X) + off)), xv);
 #pragma unroll
       for (int c = 0; c < VEC; ++c) out[c] = fma(kx, xv[c], fma(ks, sv[c], kacc * acc[c]));
-      *reinterpret_cast<V*>(static_cast<T*>(a.O) + off) = VT::make(out);
+      V* op = reinterpret_cast<V*>(static_cast<T*>(a.O) + off);
+      if constexpr (OUT_EF)
+        __stcs(op, VT::make(out));
+      else
+        *op = VT::make(out);
     }
   }
 }
@@ -477,6 +484,7 @@ template <typename T, int LPR, int MINB = (LPR == 16 ? 6 : 8)>
 static int launch_mid(const StepArgs& a, int device, cudaStream_t s) {
   const bool unit = a.wv == nullptr;
   auto kern = unit ? k_cheb_mid<T, LPR, MINB, true> : k_cheb_mid<T, LPR, MINB, false>;
+  if (a.pol) kern = unit ? k_cheb_mid<T, LPR, MINB, true, true> : k_cheb_mid<T, LPR, MINB, false, true>;
   // per (device, unit) occupancy, published atomically: concurrent host threads (the CG
   // overlap worker) either see 0 and compute the same value or read the stored one
   static std::atomic<int> occ_cache[64][2];
@@ -605,6 +613,7 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   StepArgs a = a_in;
   a.hints = g_opt.cache_hints.load() != 0;
   a.contig = g_opt.row_order.load() == 1;
+  a.pol = (int)g_opt.l2_policy.load();
   constexpr int VEC = 16 / sizeof(T);
   if (pw < VEC || pw % VEC != 0 || pw > 32 * VEC) fail(CSC_ERR_INVALID, "unsupported panel width");
   a.sv = pw / VEC;
@@ -869,7 +878,7 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz, bool
       // 6.04 -> 7.64 ms) keep one panel (profiles/r02_ab_two_panels.txt)
       const double l2 = (double)device_props(device).l2_bytes;
       const int p128 = 128 / (int)dtype_size(dtype);
-      if (dtype == CSC_F32 && pw > p128 && (double)n * pw * dtype_size(dtype) > l2 && (double)n * 128.0 <= l2)
+      if (dtype == CSC_F32 && one > p128 && (double)n * one * dtype_size(dtype) > l2 && (double)n * 128.0 <= l2)
         pw = p128;
     }
     max_pw = std::min(pw, max_pw);

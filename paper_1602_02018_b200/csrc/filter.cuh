@@ -75,6 +75,7 @@ struct StepArgs {
   int sv;        // panel row stride in 16-B vectors = pw / VEC (set by launch_step); the
                  // kernel's lanes per row are the next power of two, lanes >= sv idle
   int contig;    // contiguous row ranges per warp (set by launch_step)
+  int pol;       // k_cheb_mid L2 policy bits (option l2_policy, set by launch_step)
   // row-sharded peer transport (rows.cu): O's rows are also stored into every rank's next
   // gather panel, peers[q] + (peer_row0 + row) * pw, over NVLink -- the all-gather fused
   // into the step.  npeers = 0: off.
