@@ -355,3 +355,32 @@ def test_features_async_device_call_matches(c1_golden):
     assert P.features.features_into(op, low, X, F1, zero_rows=False) is None
     torch.cuda.synchronize()
     assert z.size == 0 and torch.equal(F0, F1)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_overlapped_host_upload_bit_identical(c1_golden, dtype):
+    """Multi-panel blocks in pinned host memory are uploaded panel by panel on a copy stream,
+    narrowest panel first, each packed when its filter starts (option h2d_overlap): features,
+    filter output and eigencount are the same bytes as the one-copy path."""
+    import torch
+
+    from paper_1602_02018_b200.spectrum import eigencount
+
+    g, _ = c1_graph()
+    op = P.laplacian_op(g, dtype=dtype)
+    low = P.design_lowpass(0.4, 50)
+    narrow = 8 if dtype == "float32" else 4
+    X = torch.empty((g.num_nodes, 31), dtype=torch.float64).pin_memory().numpy()
+    X[:] = np.random.default_rng(17).standard_normal(X.shape)
+    out = {}
+    for ov in (0, 1):
+        with options(h2d_overlap=ov, panel_width=narrow):
+            F = torch.empty(X.shape, dtype=torch.float64).pin_memory().numpy()
+            z = P.features.features_into(op, low, X, F)
+            Y = P.apply_filter(low, op, X)
+            cnt = eigencount(op, 0.4, rng=np.random.default_rng(3), num_signals=31, _signals=X)
+            out[ov] = (F.copy(), z, Y, cnt.count)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1].tolist() == out[1][1].tolist()
+    assert np.array_equal(out[0][2], out[1][2])
+    assert out[0][3] == out[1][3]
