@@ -522,6 +522,11 @@ def run_ours(args, cfg):
         "algorithmic_unit": f"SURVEY.md 8(d) B_step(w) = B_csr + 5 N w s per step launch (B_first on the first), "
                             f"w = {w_local} columns of rank 0; one launch per step when the block is one panel",
         "kernel_stream_bytes_per_launch": step_bytes / max(step_launches, 1),
+        # the DRAM-traffic-limited ceiling: frac if the kernel moved its measured (ncu) DRAM
+        # traffic at the copy peak; the gap to 1 is gather misses, not kernel inefficiency
+        "traffic_ceiling_frac": (alg_per_filter * args.steps / max(step_launches, 1)) / traffic if traffic else None,
+        "achieved_of_traffic_ceiling": ((achieved / peak) / ((alg_per_filter * args.steps / max(step_launches, 1))
+                                                              / traffic)) if traffic and achieved else None,
         "frac_of_8tbs": (achieved / 8000.0) if achieved else None,  # report against both peaks
         "ncu_dram_throughput_pct": _ncu_dram_pct(args.config, cfg["dtype"]) if world == 1 and rop is None else None,
         "ncu_dram_gbs": _ncu_dram_gbs(args.config, cfg["dtype"]) if world == 1 and rop is None else None,
