@@ -13,6 +13,7 @@
 // Replicates run concurrently on separate SMs; the host picks the lowest inertia
 // (first minimum, kmeans.py:121-123).  A replicate whose D^2 total is not positive
 // (the reference's rng.integers fallback, kmeans.py:57-58) is flagged for the host.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -197,12 +198,53 @@ __device__ double sqdiff_col(const double* a, const double* C, int64_t k, int j,
   }, 0, d);
 }
 
+// sqdiff_col evaluated by the 8 lanes of an octet (8 <= d <= 128, pw_leaf's case): lane o
+// keeps pw_leaf's accumulator r[o] (its coordinates o, o + 8, ... in order), the tree
+// ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) is built with xor shuffles (a + b == b + a
+// exactly), and the d % 8 tail is added in order -- bit-identical to sqdiff_col, with the
+// point's row read coalesced.  Every lane of the octet returns the sum.
+__device__ double sqdiff_col_oct(const double* a, const double* C, int64_t k, int j, int d, int o) {
+  const int n8 = d - d % 8;
+  auto v = [a, C, k, j](int t) {
+    const double u = __dsub_rn(a[t], C[(int64_t)t * k + j]);
+    return __dmul_rn(u, u);
+  };
+  double r = v(o);
+  for (int i = 8; i < n8; i += 8) r = __dadd_rn(r, v(i + o));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+  for (int i = n8; i < d; ++i) r = __dadd_rn(r, v(i));
+  return r;
+}
+
+// seeding's D^2 update near[i] (= or min=) ||p_i - c_j||^2 over all points (whole CTA)
+__device__ void d2_update(const double* __restrict__ P, int64_t n, int d, const double* C, int64_t k, int j,
+                          double* near, bool first) {
+  const int tid = threadIdx.x;
+  if (d >= 8 && d <= 128) {  // four points per warp, one octet each
+    const int lane = tid & 31, oct = lane >> 3, o = lane & 7;
+    const int64_t per = (int64_t)(blockDim.x >> 5) * 4;
+    for (int64_t base = (int64_t)(tid >> 5) * 4; base < n; base += per) {
+      const int64_t i = base + oct;
+      const double v = sqdiff_col_oct(P + (i < n ? i : n - 1) * d, C, k, j, d, o);
+      if (o == 0 && i < n) near[i] = first ? v : fmin(near[i], v);
+    }
+  } else {
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      const double v = sqdiff_col(P + i * d, C, k, j, d);
+      near[i] = first ? v : fmin(near[i], v);
+    }
+  }
+}
+
 __global__ void k_sqnorm(const double* __restrict__ X, int64_t rows, int d, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = sq_row(X + i * d, d);
 }
 
 constexpr int kThreads = 1024;
+constexpr int kQP = 4;  // points per warp in the Lloyd assignment
 
 // Byte offsets of the per-replicate arrays in dynamic shared memory (-1: global slice).
 // The seeding walks near/cdf sequentially in one thread and Lloyd scans lab per
@@ -257,7 +299,7 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
     const double* p0 = P + first[r] * d;
     for (int t = tid; t < d; t += kThreads) C[(int64_t)t * k] = p0[t];
     __syncthreads();
-    for (int64_t i = tid; i < n; i += kThreads) near[i] = sqdiff_col(P + i * d, C, k, 0, d);
+    d2_update(P, n, d, C, k, 0, near, true);
     __syncthreads();
     for (int j = 1; j < k; ++j) {
       const double total_all = pw_sum_block([near](int64_t i) { return near[i]; }, n, s_plan, s_leaf);
@@ -305,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
       const double* pj = P + s_pick * d;
       for (int t = tid; t < d; t += kThreads) C[(int64_t)t * k + j] = pj[t];
       __syncthreads();
-      for (int64_t i = tid; i < n; i += kThreads) near[i] = fmin(near[i], sqdiff_col(P + i * d, C, k, j, d));
+      d2_update(P, n, d, C, k, j, near, false);
       __syncthreads();
     }
   } else {
@@ -326,43 +368,68 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rep(
         counts[j] = 0;
       }
       __syncthreads();
-      // assignment: one warp per point, lanes over centroids, first argmin
-      double* p = pbuf + (size_t)warp * d;
-      for (int64_t i = warp; i < n; i += kThreads / 32) {
-        for (int t = lane; t < d; t += 32) p[t] = P[i * d + t];
+      // assignment: four points per warp (kQP), lanes over centroids, first argmin.  Each
+      // (point, centroid) distance is the same sequential fma chain over the coordinates as
+      // one point per warp; a centroid coordinate loaded once serves the four points, and the
+      // points sit coordinate-major in pbuf ([t][q]: two 16-B broadcast loads per t).
+      double* p4 = pbuf + (size_t)warp * kQP * d;
+      for (int64_t i0 = (int64_t)warp * kQP; i0 < n; i0 += (int64_t)(kThreads / 32) * kQP) {
+        for (int u = lane; u < kQP * d; u += 32) {  // the four rows are contiguous in P
+          const int q = u / d, t = u - q * d;
+          p4[t * kQP + q] = i0 + q < n ? P[i0 * d + u] : 0.0;
+        }
         __syncwarp();
-        double best = INFINITY;
-        int bj = 0;
+        double best[kQP], ppi[kQP];
+        int bj[kQP];
+#pragma unroll
+        for (int q = 0; q < kQP; ++q) {
+          best[q] = INFINITY;
+          bj[q] = 0;
+          ppi[q] = i0 + q < n ? pp[i0 + q] : 0.0;
+        }
         for (int j0 = 0; j0 < k; j0 += 32) {
           const int j = j0 + lane;
-          double dist = INFINITY;
-          if (j < k) {
-            double dot = 0.0;  // C is d x k: the warp's 32 centroids are contiguous per coordinate
-            for (int t = 0; t < d; ++t) dot = fma(p[t], C[(int64_t)t * k + j], dot);
-            dist = fmax(__dsub_rn(__dadd_rn(pp[i], cc[j]), 2.0 * dot), 0.0);
-          }
-          double v = dist;
-          int vj = j < k ? j : INT_MAX;
+          double dot[kQP];
 #pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-            const int oj = __shfl_xor_sync(0xffffffffu, vj, o);
-            if (ov < v || (ov == v && oj < vj)) {
-              v = ov;
-              vj = oj;
+          for (int q = 0; q < kQP; ++q) dot[q] = 0.0;
+          if (j < k) {  // C is d x k: the warp's 32 centroids are contiguous per coordinate
+            for (int t = 0; t < d; ++t) {
+              const double c = C[(int64_t)t * k + j];
+              const double2 pa = *reinterpret_cast<const double2*>(p4 + t * kQP);
+              const double2 pb = *reinterpret_cast<const double2*>(p4 + t * kQP + 2);
+              dot[0] = fma(pa.x, c, dot[0]);
+              dot[1] = fma(pa.y, c, dot[1]);
+              dot[2] = fma(pb.x, c, dot[2]);
+              dot[3] = fma(pb.y, c, dot[3]);
             }
           }
-          if (v < best) {  // strictly smaller: earlier chunks keep ties
-            best = v;
-            bj = vj;
+#pragma unroll
+          for (int q = 0; q < kQP; ++q) {
+            double v = j < k ? fmax(__dsub_rn(__dadd_rn(ppi[q], cc[j]), 2.0 * dot[q]), 0.0) : INFINITY;
+            int vj = j < k ? j : INT_MAX;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+              const int oj = __shfl_xor_sync(0xffffffffu, vj, o);
+              if (ov < v || (ov == v && oj < vj)) {
+                v = ov;
+                vj = oj;
+              }
+            }
+            if (v < best[q]) {  // strictly smaller: earlier chunks keep ties
+              best[q] = v;
+              bj[q] = vj;
+            }
           }
         }
-        if (lane == 0) {
-          lab[i] = bj;
-          near[i] = best;
-          atomicAdd(&counts[bj], 1);
-        }
-        __syncwarp();  // p is overwritten by the next point
+#pragma unroll
+        for (int q = 0; q < kQP; ++q)
+          if (lane == q && i0 + q < n) {
+            lab[i0 + q] = bj[q];
+            near[i0 + q] = best[q];
+            atomicAdd(&counts[bj[q]], 1);
+          }
+        __syncwarp();  // p4 is overwritten by the next points
       }
       __syncthreads();
       const double inert_all = pw_sum_block([near](int64_t i) { return near[i]; }, n, s_plan, s_leaf);
@@ -450,9 +517,14 @@ void run_replicates(const double* points, int64_t n, int d, int k, int reps, con
   DeviceView dPcg(pcg, first ? sizeof(uint64_t) * 4 * reps : 0, device, s);
   DeviceView dInit(first ? nullptr : init, first ? 0 : sizeof(double) * reps * k * d, device, s);
   const size_t c_bytes = sizeof(double) * k * d;
-  const size_t limit = 200 * 1024;
+  // dynamic shared memory: the opt-in per-block maximum less the kernel's static arrays
+  cudaFuncAttributes fa;
+  CSC_CUDA(cudaFuncGetAttributes(&fa, k_kmeans_rep));
+  int optin = 0;
+  CSC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  const size_t limit = (size_t)std::max<int64_t>(0, (int64_t)optin - (int64_t)fa.sharedSizeBytes - 1024);
   SmemPlan sp;
-  sp.bytes = (((size_t)k * 16 + 15) / 16) * 16 + sizeof(double) * (kThreads / 32) * d;  // cc, counts, offs, points
+  sp.bytes = (((size_t)k * 16 + 15) / 16) * 16 + sizeof(double) * (kThreads / 32) * kQP * d;  // cc, counts, offs, points
   if (sp.bytes > limit) fail(CSC_ERR_INVALID, "kmeans: k or d too large for the device kernel");
   auto place = [&](int64_t& off, size_t bytes) {
     bytes = (bytes + 15) / 16 * 16;

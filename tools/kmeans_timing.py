@@ -1,4 +1,5 @@
-"""Time the device k-means (all replicates) on C3-shaped reduced features (n=922, d=56, k=100)."""
+"""Time the device k-means (all replicates) on C3-shaped reduced features (n=922, d=56, k=100),
+or on a headline capture's real reduced features: python tools/kmeans_timing.py [c4|c3]."""
 import sys
 import time
 from pathlib import Path
@@ -10,10 +11,16 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1602_02018_b200 as P  # noqa: E402
 
 rng = np.random.default_rng(0)
-k, n, d = 100, 922, 56
-centers = rng.standard_normal((k, d))
-pts = centers[rng.integers(k, size=n)] + 0.3 * rng.standard_normal((n, d))
-pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+if len(sys.argv) > 1:
+    gz = np.load(Path(__file__).resolve().parents[1] / "tests" / "golden" / f"pipeline_{sys.argv[1]}.npz")
+    pts = np.ascontiguousarray(gz["reduced_features"])
+    n, d = pts.shape
+    k = int(gz["truth"].max()) + 1
+else:
+    k, n, d = 100, 922, 56
+    centers = rng.standard_normal((k, d))
+    pts = centers[rng.integers(k, size=n)] + 0.3 * rng.standard_normal((n, d))
+    pts /= np.linalg.norm(pts, axis=1, keepdims=True)
 cfg = P.KmeansConfig(k=k, seed=3)
 P.kmeans(pts, cfg)
 for _ in range(3):
@@ -46,7 +53,7 @@ def run(R, max_iters):
 
 
 for R in (1, 20):
-    for mi in (0, 100):
+    for mi in (0, 300):
         run(R, mi)
         t, it = run(R, mi)
         print(f"replicates {R:2d} max_iters {mi:3d}: {t:7.2f} ms (max iterations {it})", flush=True)
