@@ -366,6 +366,16 @@ def run_ours(args, cfg):
                             f"{world} rank(s), graph replicated; max over ranks; median of 3 warm calls")
                    if sharded else ("full run_csc in parity mode (numpy's seeded streams reproduced on the GPU), "
                                     "graph resident; median of 3 warm calls")}
+            # the reference's own run_csc on this config, recorded when the golden capture was made
+            # (tests/golden/make_golden.py, one core): its wall time and whether our labels match it
+            cap = ROOT / "tests" / "golden" / f"pipeline_{args.config}.npz"
+            gz = np.load(cap) if cap.exists() and world == 1 else None
+            if gz is not None and "wall_s" in gz.files:
+                csc["reference_capture"] = {
+                    "wall_s": float(gz["wall_s"]), "stages_s": json.loads(str(gz["timings"])),
+                    "lambda_k_hat": float(gz["lambda_k_hat"]),
+                    "labels_ari_vs_reference": P.adjusted_rand_index(res.labels, gz["labels"]),
+                    "source": f"tests/golden/pipeline_{args.config}.npz (reference run_csc, fp64, 1 core, build container)"}
         except Exception as exc:  # secondary: never lose the metric line over it
             csc = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         del res

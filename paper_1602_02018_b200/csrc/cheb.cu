@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
   // size): fewer registers in the neighbour loop
   const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
-  const uint32_t SV = (uint32_t)a.sv;  // row stride in vectors (<= LPR; == LPR unless the panel is tight)
+  constexpr uint32_t SV = LPR;  // row stride in vectors
   const V* __restrict__ Gv = static_cast<const V*>(a.G) + sub;
 
   const T* __restrict__ G = static_cast<const T*>(a.G);
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
   const int n = (int)a.n;
   const int ngroups = (n + GPW - 1) / GPW;
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
-  const uint32_t SV = (uint32_t)a.sv;  // row stride in vectors (<= LPR)
+  constexpr uint32_t SV = LPR;  // row stride in vectors
   const V* __restrict__ Gv = static_cast<const V*>(a.G) + sub;
   const T ka = static_cast<T>(a.ka), ks = static_cast<T>(a.ks), kx = static_cast<T>(a.kx);
   int gi = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -845,7 +845,7 @@ template int filter_panel<double>(const csc_graph*, const double*, int, const do
 
 // ---------------------------------------------------------------------------
 // panels
-PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz, bool tight) {
+PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
   const int vec = 16 / (int)dtype_size(dtype);
   const int max_lpr = 32;
   int max_pw = vec * max_lpr;
@@ -892,8 +892,6 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz, bool
     int pw;
     if (rem >= max_pw) {
       pw = max_pw;
-    } else if (tight) {
-      pw = (rem + vec - 1) / vec * vec;
     } else {
       pw = vec;
       while (pw < rem) pw *= 2;
@@ -1290,7 +1288,7 @@ struct PackedInput {
   std::vector<int> order;  // panel processing order
   PackedInput(const csc_graph* g, const void* src, int64_t ld, int ncols, int io, cudaStream_t s, bool lazy = false)
       : g_(g), io_(io), s_(s) {
-    pp = plan_panels(g->n, ncols, g->dtype, g->device, g->nnz, g_opt.tight_panels.load() != 0);
+    pp = plan_panels(g->n, ncols, g->dtype, g->device, g->nnz);
     const size_t cs = dtype_size(g->dtype);
     for (int j = 0; j < pp.np; ++j) order.push_back(j);
     x.alloc(cs * pp.total, s);

@@ -72,10 +72,9 @@ struct StepArgs {
   int fwd;       // forward-mode accumulate
   int last;      // symmetric-basis output + isolated-node fixup (+ epilogue)
   int hints;     // evict-first hints on streamed operands (set by launch_step)
-  int sv;        // panel row stride in 16-B vectors = pw / VEC (set by launch_step); the
-                 // kernel's lanes per row are the next power of two, lanes >= sv idle
+  int sv;        // panel row stride in 16-B vectors = pw / VEC = lanes per row (set by launch_step)
   int contig;    // contiguous row ranges per warp (set by launch_step)
-  int pol;       // k_cheb_mid L2 policy bits (option l2_policy, set by launch_step)
+  int pol;       // output panel stored evict-first (option l2_policy, set by launch_step)
   // row-sharded peer transport (rows.cu): O's rows are also stored into every rank's next
   // gather panel, peers[q] + (peer_row0 + row) * pw, over NVLink -- the all-gather fused
   // into the step.  npeers = 0: off.
@@ -94,10 +93,10 @@ struct PanelPlan {
   int max_pw = 0;
 };
 
-// tight: the last (or only) panel is w rounded up to one 16-B vector instead of a power of
-// two (C3's d = 56 fp32 block: 224-B rows, not 256-B), so no padding columns are streamed
-// or gathered; the kernels then run pow2 lanes per row with the tail lanes idle.
-PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz, bool tight = false);
+// Panel widths are powers of two (x 16-B vectors); rows rounded to 16 B instead ("tight"
+// panels, 224-B rows for C3's d = 56) were measured slower at C3 and removed
+// (profiles/r02_ab_tight_panels.txt).
+PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz);
 
 // Upper bound of the step kernel's grid (for sizing epilogue partials).
 int step_grid_cap(int device);

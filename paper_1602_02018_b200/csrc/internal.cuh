@@ -78,7 +78,6 @@ struct Options {
   std::atomic<int64_t> cg_overlap{1};     // block CG: two panels at a time (0 off, 1 auto, 2 no width token)
   std::atomic<int64_t> lean_mid{1};       // K2: lean mid-step kernel (k_cheb_mid) where it applies
   std::atomic<int64_t> fast_normalize{1}; // K3: vectorised single-panel row normalisation
-  std::atomic<int64_t> tight_panels{0};   // filter panels: last panel w rounded to 16 B, not a power of 2 (A/B: off)
   std::atomic<int64_t> h2d_overlap{1};    // filters of multi-panel pinned host blocks: per-panel uploads overlap
   std::atomic<int64_t> l2_policy{1};      // step kernels: output panel stored evict-first (1) or write-back (0)
 };

@@ -343,8 +343,7 @@ void run_rows(const std::vector<const csc_graph*>& gs, csc_comm* cm, csc_peers* 
   int64_t nnz_all = 0;
   for (const csc_graph* g : gs) nnz_all += g->nnz;
   if (gs.size() == 1) nnz_all = g0->nnz * nranks;  // one rank of many: estimate
-  const PanelPlan pp = plan_panels(g0->gather_rows, ncols, g0->dtype, g0->device, nnz_all,
-                                   g_opt.tight_panels.load() != 0);
+  const PanelPlan pp = plan_panels(g0->gather_rows, ncols, g0->dtype, g0->device, nnz_all);
   if (pe && sizeof(T) * (size_t)R * nranks * pp.max_pw > pe->panel_bytes)
     fail(CSC_ERR_INVALID, "peer panels too small for this block (see csc_panel_row_bytes)");
   const int cap = step_grid_cap(g0->device);
@@ -592,7 +591,7 @@ int csc_cheb_filter_rows_group(const csc_graph* const* shards, int nshards, cons
 int csc_panel_row_bytes(int64_t num_nodes, int ncols, int dtype, int device, int64_t nnz, int64_t* out) {
   return guard([&] {
     if (!out || num_nodes < 1 || ncols < 1) fail(CSC_ERR_INVALID, "bad arguments");
-    const PanelPlan pp = plan_panels(num_nodes, ncols, dtype, device, nnz, g_opt.tight_panels.load() != 0);
+    const PanelPlan pp = plan_panels(num_nodes, ncols, dtype, device, nnz);
     *out = (int64_t)pp.max_pw * (int64_t)dtype_size(dtype);
   });
 }

@@ -178,7 +178,6 @@ static std::atomic<int64_t>* option_slot(const char* key) {
   if (k == "cg_overlap") return &g_opt.cg_overlap;
   if (k == "lean_mid") return &g_opt.lean_mid;
   if (k == "fast_normalize") return &g_opt.fast_normalize;
-  if (k == "tight_panels") return &g_opt.tight_panels;
   if (k == "l2_policy") return &g_opt.l2_policy;
   if (k == "h2d_overlap") return &g_opt.h2d_overlap;
   if (k == "block_threads") return &g_opt.block_threads;

@@ -15,8 +15,12 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--dtype", default=None)
 ap.add_argument("--option", action="append", default=[], help="libcsc option key=value")
+ap.add_argument("--lib", default=None, help="another build of libcsc_b200.so (A/B)")
 args = ap.parse_args()
 from paper_1602_02018_b200 import _lib  # noqa: E402
+
+if args.lib:
+    _lib.LIB_PATH = Path(args.lib).resolve()
 
 for kv in args.option:
     key, val = kv.split("=")
