@@ -881,6 +881,13 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
       const int p128 = 128 / (int)dtype_size(dtype);
       if (dtype == CSC_F32 && one > p128 && (double)n * one * dtype_size(dtype) > l2 && (double)n * 128.0 <= l2)
         pw = p128;
+      // ... and in the DRAM-random regime (gather source > 4x L2, C5), where a gathered row
+      // costs per 128-B line, a block just over 128 B runs as one 128-B-row panel plus a narrow
+      // remainder rather than one 256-B-row panel (C5 probe, 34 columns: 496 -> 401 ms per
+      // filter, profiles/r02_c5_panels.txt)
+      if (dtype == CSC_F32 && one > p128 && (double)n * one * dtype_size(dtype) > 4.0 * l2 &&
+          (size_t)(w - p128) * dtype_size(dtype) <= 32)
+        pw = p128;
     }
     max_pw = std::min(pw, max_pw);
   }

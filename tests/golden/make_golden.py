@@ -6,7 +6,7 @@ not shipped to the GPU box):
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
         python tests/golden/make_golden.py [--c2] [--c3] [--c4]
 
---c3 / --c4 run the reference's run_csc ONCE at the headline configs (C3: SBM N=1e6,
+--c2cap / --c3 / --c4 run the reference's run_csc ONCE at BASELINE configs 2-4 (C3: SBM N=1e6,
 k=100, d=56, ~1-2 h of one CPU core; C4: the repo's DC-SBM graph, N=334,863, k=250,
 d=51, fed through the reference's build_graph) and capture every stage's output by
 wrapping the stage functions run_csc binds by name (pipeline.py:19-26), the seam the
@@ -270,10 +270,16 @@ def edgelists():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
+    ap.add_argument("--c2cap", action="store_true", help="stage capture at C2 (pipeline_c2cap.npz, ~2.5 min)")
     ap.add_argument("--c3", action="store_true")
     ap.add_argument("--c4", action="store_true")
     ap.add_argument("--only", action="store_true", help="skip the small fixtures")
     args = ap.parse_args()
+    if args.c2cap:
+        N, k = 100_000, 20
+        g, truth = ref.sbm_generate(sbm_config(N, k))
+        out = capture_run(g, truth, k, int(math.ceil(4 * math.log(N))), 0, "c2")
+        np.savez_compressed(OUT / "pipeline_c2cap.npz", **out)
     if args.c3:
         N, k = 1_000_000, 100
         g, truth = ref.sbm_generate(sbm_config(N, k))

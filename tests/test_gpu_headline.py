@@ -1,4 +1,5 @@
-"""run_csc at the headline configs (BASELINE C3: SBM N=1e6, k=100; C4: DC-SBM N=334,863, k=250)
+"""run_csc at BASELINE C2 (SBM N=1e5, k=20), the headline C3 (SBM N=1e6, k=100) and C4 (DC-SBM
+N=334,863, k=250)
 against the REAL reference's run_csc on the same graph, seed and d (tests/golden/make_golden.py
 --c3 / --c4, which wraps the stage functions reference pipeline.py:19-26 binds by name).
 
@@ -37,7 +38,9 @@ _graphs: dict = {}
 def _graph(tag):
     if tag not in _graphs:
         _graphs.clear()
-        if tag == "c3":
+        if tag == "c2cap":
+            _graphs[tag] = P.sbm_generate(sbm_config(100_000, 20))
+        elif tag == "c3":
             _graphs[tag] = P.sbm_generate(sbm_config(1_000_000, 100))
         else:
             from paper_1602_02018_b200.sbm import c4_config
@@ -81,7 +84,7 @@ def _captured_run(op, params, rows):
     return res, cap
 
 
-@pytest.mark.parametrize("tag", ["c3", "c4"])
+@pytest.mark.parametrize("tag", ["c2cap", "c3", "c4"])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_run_csc_headline_matches_reference(tag, dtype):
     if not (GOLDEN / f"pipeline_{tag}.npz").exists():
