@@ -69,6 +69,19 @@ def main():
           f"gaps {gaps / 1e3 / args.steps:.3f} ms/step")
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
         print(f"  {v / 1e3 / args.steps:8.3f} ms/step  {cnt[k] // args.steps:4d}/step  {k}")
+    # idle time: the span minus the union of all (possibly concurrent) device intervals, and
+    # the largest idle intervals with the work on either side
+    idle = []
+    end, last = evs[0].time_range.end, evs[0]
+    for e in evs[1:]:
+        if e.time_range.start > end:
+            idle.append((e.time_range.start - end, last.name[:50], e.name[:50], end - evs[0].time_range.start))
+        if e.time_range.end > end:
+            end, last = e.time_range.end, e
+    print(f"idle (span - union of device intervals): {sum(i[0] for i in idle) / 1e3 / args.steps:.3f} ms/step in "
+          f"{len(idle)} intervals")
+    for us, a, b, at in sorted(idle, reverse=True)[:15]:
+        print(f"  {us:9.1f} us at {at / 1e3:9.3f} ms  after {a}  before {b}")
 
 
 if __name__ == "__main__":
