@@ -392,6 +392,20 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     nbeg = __ldg(a.indptr + gi * GPW + grp);
     nend = __ldg(a.indptr + gi * GPW + grp + 1);
   }
+  // the first chunk's column indices (and weights) of the warp's next row group, loaded one
+  // group ahead so a group starts with its gathers instead of an index round trip
+  int32_t jf[UC];
+  T wf[UC];
+  auto first_chunk = [&]() {
+#pragma unroll
+    for (int u = 0; u < UC; ++u) {  // slot k of a chunk is entry k / LPR of lane k % LPR
+      const int e = u * LPR + sub;
+      const bool ok = e < nend - nbeg && (UC > 1 || sub < CH);
+      jf[u] = ok ? __ldcs(a.indices + nbeg + e) : -1;
+      if constexpr (!UNIT) wf[u] = ok ? __ldcs(static_cast<const T*>(a.wv) + nbeg + e) : T(0);
+    }
+  };
+  first_chunk();
   for (; gi < ngroups; gi += nwarps) {
     const int row = gi * GPW + grp;
     const int cnt = nend - nbeg;
@@ -405,11 +419,9 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
       int32_t jj[UC];
       T ww[UC];
 #pragma unroll
-      for (int u = 0; u < UC; ++u) {  // slot k of a chunk is entry k / LPR of lane k % LPR
-        const int e = u * LPR + sub;
-        const bool ok = e < cnt && (UC > 1 || sub < CH);
-        jj[u] = ok ? __ldcs(ip + e) : -1;
-        if constexpr (!UNIT) ww[u] = ok ? __ldcs(wp + e) : T(0);
+      for (int u = 0; u < UC; ++u) {
+        jj[u] = jf[u];
+        if constexpr (!UNIT) ww[u] = wf[u];
       }
       for (int base = 0; base < maxcnt; base += CH) {
         int32_t jn[UC];
@@ -459,6 +471,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
         nbeg = nend = 0;
       }
     }
+    first_chunk();  // (nbeg / nend now belong to the next group)
     if (row < n && lane_on) {
       const uint32_t off = ((uint32_t)row * SV + sub) * VEC;
       const T si = static_cast<const V2*>(a.rs)[row].x;
