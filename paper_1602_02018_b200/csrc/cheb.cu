@@ -492,9 +492,10 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
   }
 }
 
-// 256-B rows: 6 CTAs/SM at 40 registers (five gathers in flight per lane) measured 1 % faster
-// than 8 CTAs at 32; narrower rows prefer 8 CTAs (1 % the other way)
-template <typename T, int LPR, int MINB = (LPR == 16 ? 6 : 8)>
+// 6 CTAs/SM at 40 registers (five gathers in flight per lane) vs 8 CTAs at 32 (three): 64-, 256-
+// and 512-B rows are faster with 6 (C3 16 columns -4.8 %, C4 k = 250 -8 %), 128-B rows with 8
+// (C3 features +1.4 % with 6), 16-B rows keep 8 (profiles/r02_ab_minb.txt)
+template <typename T, int LPR, int MINB = (LPR == 8 || LPR == 1 ? 8 : 6)>
 static int launch_mid(const StepArgs& a, int device, cudaStream_t s) {
   const bool unit = a.wv == nullptr;
   auto kern = unit ? k_cheb_mid<T, LPR, MINB, true> : k_cheb_mid<T, LPR, MINB, false>;
