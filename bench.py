@@ -66,6 +66,21 @@ def filter_bytes(N: int, nnz: int, w: int, s: int, p: int) -> float:
     return (b_csr + 3.0 * N * w * s) + (p - 1) * (b_csr + 5.0 * N * w * s)
 
 
+def _l2_path(step_ms, step_bytes, steps, n, nnz, w, s, c3_f32):
+    """Bytes K2 moves from L2 to the SMs per second: the row streams of its launches plus every
+    neighbour row it gathers (nnz x w x s per step, against one compulsory read in the HBM unit)."""
+    if not step_ms or not step_bytes:
+        return None
+    per_filter = step_bytes / steps - P_ORDER * n * w * s + P_ORDER * nnz * w * s
+    ach = per_filter * steps / (step_ms / 1e3) / 1e9
+    # gathers alone on the C3 graph, 128-B rows, 64 warps/SM: 117.44 G rows/s x 128 B (r01_gather_sol.txt)
+    ceil = 117.44 * 128.0 if c3_f32 else None
+    return {"achieved_gbs": ach, "bytes_per_filter": per_filter, "gather_only_ceiling_gbs": ceil,
+            "frac_of_gather_ceiling": ach / ceil if ceil else None,
+            "note": "row streams + nnz x w x s gathered bytes per step over the K2 launch time; ceiling = "
+                    "one step's gathers alone (no streams, no epilogue) on the same graph"}
+
+
 def _ncu_dram_pct(config: str, dtype: str):
     """ncu gpu__dram_throughput (% of ncu's peak) of the K2 launches, from profiles/ncu_traffic.json."""
     tf = ROOT / "profiles" / "ncu_traffic.json"
@@ -543,6 +558,10 @@ def run_ours(args, cfg):
         "kernel_share_of_step": (step_ms / args.steps) / ms if ms > 0 else None,
         "recurrence": "clenshaw" if _lib.get_option("recurrence") == 0 or rop is not None else "forward",
         "panel_plan": _lib.get_option("panel_width") or "auto",
+        # the L2 -> SM path that bounds K2 (profiles/r02_k2_decomposition.txt): every launch moves
+        # its row streams plus deg x (row bytes) of neighbour gathers through L2
+        "l2_path": _l2_path(step_ms, step_bytes, args.steps, n_rows, nnz_rows, w_local, s_bytes,
+                            args.config == "c3" and cfg["dtype"] == "float32" and world == 1 and rop is None),
         "gather_sol_us_per_step": ({"warps_48": 302.0, "warps_64": 253.0,
                                     "source": "one step's neighbour-row gathers alone on the C3 graph "
                                               "(tools/microbench/csr_gather_sol.cu, profiles/r01_gather_sol.txt)"}
