@@ -348,6 +348,16 @@ int csc_panel_row_bytes(int64_t num_nodes, int ncols, int dtype, int device, int
 int csc_peers_create(int nranks, int rank, int device, size_t panel_bytes, csc_peers** out);
 int csc_peers_handle(const csc_peers* peers, uint8_t* out /* CSC_PEER_HANDLE_BYTES */);
 int csc_peers_attach(csc_peers* peers, int peer_rank, const uint8_t* handle);
+/* Step boundary through the host instead of the device flag barrier: when fn is set,
+ * csc_cheb_filter_rows_peers synchronises its stream after each step (the peer stores have
+ * landed) and calls fn(ctx), which must return 0 once every rank has arrived (e.g. a
+ * torch.distributed / MPI barrier); non-zero fails the call (CSC_ERR_INVALID).  For ranks
+ * that cannot run concurrently -- several processes time-sliced on one GPU, where a kernel
+ * spinning on another rank's flag may never see it -- and for checking the IPC mapping and
+ * the fused peer stores across processes.  fn = NULL restores the device barrier.  Every
+ * rank of a transport must make the same choice. */
+typedef int (*csc_host_barrier_fn)(void* ctx);
+int csc_peers_set_host_barrier(csc_peers* peers, csc_host_barrier_fn fn, void* ctx);
 int csc_peers_destroy(csc_peers* peers);
 
 /* csc_cheb_filter_rows over the peer transport: each mid step's epilogue stores

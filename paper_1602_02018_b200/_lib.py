@@ -73,6 +73,7 @@ SIGNATURES: dict[str, list] = {
     "csc_peers_create": [_i32, _i32, _i32, C.c_size_t, _p],
     "csc_peers_handle": [_p, _p],
     "csc_peers_attach": [_p, _i32, _p],
+    "csc_peers_set_host_barrier": [_p, _p, _p],
     "csc_peers_destroy": [_p],
     "csc_cheb_filter_rows_peers": [_p, _p, _p, _i32, _p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p],
     "csc_comm_unique_id": [_p],

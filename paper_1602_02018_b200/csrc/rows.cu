@@ -97,6 +97,11 @@ struct csc_peers {
   void** dptrs = nullptr;      // device: [2][nranks] panel pointers + [nranks] flag pointers
   uint64_t epoch = 0;
   bool ready = false;
+  // optional host-side barrier (csc_peers_set_host_barrier): the step boundary becomes
+  // stream synchronise + callback instead of the flag kernel, so no kernel waits on another
+  // rank's kernel (ranks of different processes time-sliced on one GPU)
+  csc_host_barrier_fn host_barrier = nullptr;
+  void* host_barrier_ctx = nullptr;
 };
 
 namespace csc {
@@ -251,6 +256,11 @@ __global__ void k_peer_barrier(void* const* flag_ptrs, int nranks, int rank, uin
 
 void peer_barrier(csc_peers* pe, cudaStream_t s) {
   ++pe->epoch;
+  if (pe->host_barrier) {
+    CSC_CUDA(cudaStreamSynchronize(s));  // this rank's peer stores have landed
+    if (pe->host_barrier(pe->host_barrier_ctx) != 0) fail(CSC_ERR_INVALID, "host barrier callback failed");
+    return;
+  }
   k_peer_barrier<<<1, 32, 0, s>>>(pe->dptrs + 2 * pe->nranks, pe->nranks, pe->rank, pe->epoch);
   CSC_LAUNCHED();
 }
@@ -661,6 +671,14 @@ int csc_peers_attach(csc_peers* pe, int peer_rank, const uint8_t* handle) {
       CSC_CUDA(cudaMemcpy(pe->dptrs, h.data(), sizeof(void*) * h.size(), cudaMemcpyHostToDevice));
       pe->ready = true;
     }
+  });
+}
+
+int csc_peers_set_host_barrier(csc_peers* pe, csc_host_barrier_fn fn, void* ctx) {
+  return guard([&] {
+    if (!pe) fail(CSC_ERR_INVALID, "NULL argument");
+    pe->host_barrier = fn;
+    pe->host_barrier_ctx = ctx;
   });
 }
 

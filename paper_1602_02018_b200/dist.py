@@ -422,15 +422,22 @@ class RowShardedOperator:
     ``"peer"`` -- the all-gather fused into the step kernel: rows are stored straight
     into every rank's CUDA-IPC-mapped gather panel over NVLink, with a flag barrier
     between steps (csc_cheb_filter_rows_peers).  Both give the same results.
+    ``barrier`` (peer transport): ``"device"`` -- the system-scope flag barrier kernel (one
+    GPU per rank, ranks run concurrently); ``"host"`` -- stream synchronise + a barrier over
+    the group after every step (csc_peers_set_host_barrier), for ranks that share a GPU.
     """
 
     def __init__(self, graph, grp: Group, dtype: str = "float32", device: int | None = None,
-                 transport: str = "nccl", starts: np.ndarray | None = None):
+                 transport: str = "nccl", starts: np.ndarray | None = None, barrier: str = "device"):
         import torch
 
         if transport not in ("nccl", "peer"):
             raise ValueError(f"unknown transport {transport!r}")
+        if barrier not in ("device", "host"):
+            raise ValueError(f"unknown barrier {barrier!r}")
         self.transport = transport
+        self.barrier = barrier
+        self._barrier_cb = None
         self.peers = None
         self._peer_bytes = 0
         self.grp = grp
@@ -502,6 +509,21 @@ class RowShardedOperator:
             for r, hb in enumerate(handles):
                 if r != self.grp.rank:
                     _lib.call("csc_peers_attach", self.peers, r, _lib.ptr(hb))
+        if self.barrier == "host":
+            if self._barrier_cb is None:
+                self._barrier_cb = C.CFUNCTYPE(C.c_int, C.c_void_p)(self._host_barrier)
+            _lib.call("csc_peers_set_host_barrier", self.peers, self._barrier_cb, None)
+
+    def _host_barrier(self, _ctx) -> int:
+        """Called by the library between steps (its stream already synchronised)."""
+        try:
+            if self.grp.world > 1:
+                import torch.distributed as dist
+
+                dist.barrier(group=self.grp.group)
+            return 0
+        except Exception:  # the C caller turns non-zero into an error status
+            return 1
 
     def _close_peers(self) -> None:
         lib = _lib._lib

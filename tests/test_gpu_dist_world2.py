@@ -74,3 +74,82 @@ def test_device_sharded_features_match_oracle():
         assert np.array_equal(z, zero)
         assert abs(cnt - ref_cnt) <= 1e-12 * ref_cnt
     assert np.abs(F - rows).max() <= 1e-12
+
+
+def _peer_rows(grp, dtype="float64", widths=(5, 40, 7), orders=(0, 1, 2, 3, 50)):
+    """One rank of the row-sharded peer transport; ranks are separate processes on cuda:0.
+
+    The step boundary goes through the host (stream synchronise + gloo barrier), so no kernel
+    ever waits on another rank's kernel; everything else is the multi-GPU path: panels exported
+    and mapped by CUDA IPC across processes, rows stored into the other process's panels by the
+    step kernel's epilogue, ping-pong panel reuse across steps and calls.
+    """
+    import torch
+    import torch.distributed as dist
+
+    import paper_1602_02018_b200 as P
+    from paper_1602_02018_b200 import dist as D
+    from gpu_util import c1_op
+
+    g = c1_op().graph
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    rop = D.RowShardedOperator(g, grp, dtype=dtype, device=0, transport="peer", barrier="host")
+    out = {"range": (rop.begin, rop.end)}
+    for w in widths:
+        X = np.random.default_rng(w).standard_normal((1000, w))
+        Xl = torch.tensor(X[rop.begin:rop.end], dtype=tdt, device="cuda:0")
+        filt = None
+        for order in orders:
+            filt = P.design_lowpass(0.6, order) if order else P.PolyFilter(np.array([0.7]), 0.6, 0, "none", "lowpass")
+            out[("y", w, order)] = rop.apply_filter(filt, Xl).cpu().numpy()
+        out[("count", w)] = rop.eigencount(filt, Xl)
+        F, zero = rop.features(filt, Xl)
+        out[("F", w)] = F.cpu().numpy()
+        out[("zero", w)] = zero
+    torch.cuda.synchronize()
+    dist.barrier()  # nobody unmaps or frees a panel a peer may still be storing into
+    rop._close_peers()
+    dist.barrier()
+    return out
+
+
+def _peer_rows32(grp):
+    return _peer_rows(grp, dtype="float32", widths=(21,), orders=(1, 50))
+
+
+@pytest.mark.parametrize("world,fn,dtype", [(2, _peer_rows, "float64"), (3, _peer_rows, "float64"),
+                                           (2, _peer_rows32, "float32")])
+def test_row_sharded_peer_transport_across_processes(world, fn, dtype):
+    """World 2 and 3 as processes sharing cuda:0 == the replicated path, bit for bit."""
+    import torch
+
+    import paper_1602_02018_b200 as P
+    from paper_1602_02018_b200 import dist as D
+    from gpu_util import c1_op
+
+    parts = run_world(fn, world=world)
+    g = c1_op().graph
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    one = D.RowShardedOperator(g, D.Group(0, 1), dtype=dtype, transport="peer")
+    ranges = [p["range"] for p in parts]
+    assert ranges[0][0] == 0 and ranges[-1][1] == 1000 and all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    keys = [k for k in parts[0] if k != "range"]
+    for key in keys:
+        if key[0] == "y":
+            _, w, order = key
+            X = torch.tensor(np.random.default_rng(w).standard_normal((1000, w)), dtype=tdt, device="cuda")
+            filt = P.design_lowpass(0.6, order) if order else P.PolyFilter(np.array([0.7]), 0.6, 0, "none", "lowpass")
+            ref = one.apply_filter(filt, X).cpu().numpy()
+            got = np.concatenate([p[key] for p in parts])
+            assert np.array_equal(got, ref), key
+    order = max(k[2] for k in keys if k[0] == "y")
+    filt = P.design_lowpass(0.6, order)
+    for w in sorted({k[1] for k in keys if k[0] == "F"}):
+        X = torch.tensor(np.random.default_rng(w).standard_normal((1000, w)), dtype=tdt, device="cuda")
+        Fref, zref = one.features(filt, X)
+        assert np.array_equal(np.concatenate([p[("F", w)] for p in parts]), Fref.cpu().numpy())
+        assert np.array_equal(np.concatenate([p[("zero", w)] for p in parts]), zref)
+        cref = one.eigencount(filt, X)
+        for p in parts:  # every rank holds the rank-ordered sum of the partials
+            assert p[("count", w)] == parts[0][("count", w)]
+            assert abs(p[("count", w)] - cref) <= (1e-12 if dtype == "float64" else 1e-5) * cref
