@@ -92,6 +92,31 @@ struct Pair<double> {
   using type = double2;
 };
 
+// Programmatic dependent launch (sm_90+): a step kernel lets its successor in the stream be
+// scheduled at once and waits for its predecessor's completion (and memory flush) only
+// after its own CSR prologue.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// <<<grid, threads, 0, s>>> with the programmatic-stream-serialization attribute (option pdl)
+template <typename K>
+static void launch_pdl(K kern, int grid, int threads, cudaStream_t s, const StepArgs& a) {
+  if (g_opt.pdl.load() == 0) {
+    kern<<<grid, threads, 0, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CSC_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
 template <typename T, int LPR, int EPI, int CHUNK, int MINB, bool UNIT>
 __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
   using VT = Vec16<T>;
@@ -157,10 +182,12 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
   }
   int gi = gfirst;
   int32_t nbeg = 0, nend = 0;  // indptr pair of the next row group (prefetched)
+  pdl_trigger();
   if (G != nullptr && gi < glast && gi * GPW + grp < n) {
     nbeg = __ldg(a.indptr + gi * GPW + grp);
     nend = __ldg(a.indptr + gi * GPW + grp + 1);
   }
+  pdl_wait();  // earlier kernels' panels are read and written only below
   for (; gi < glast; gi += gstep) {
     const int row = gi * GPW + grp;
     const bool rok = row < n;
@@ -388,6 +415,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
   const T ka = static_cast<T>(a.ka), ks = static_cast<T>(a.ks), kx = static_cast<T>(a.kx);
   int gi = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   int32_t nbeg = 0, nend = 0;
+  pdl_trigger();
   if (gi < ngroups && gi * GPW + grp < n) {
     nbeg = __ldg(a.indptr + gi * GPW + grp);
     nend = __ldg(a.indptr + gi * GPW + grp + 1);
@@ -406,6 +434,10 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     }
   };
   first_chunk();
+  // programmatic dependent launch: everything above reads only the CSR, so it overlaps the
+  // previous step's drain; the panels written by earlier kernels are touched after the wait
+  // (a no-op for a launch without the attribute)
+  pdl_wait();
   for (; gi < ngroups; gi += nwarps) {
     const int row = gi * GPW + grp;
     const int cnt = nend - nbeg;
@@ -514,7 +546,7 @@ static int launch_mid(const StepArgs& a, int device, cudaStream_t s) {
   const int64_t rows_per_block = 8 * (32 / LPR);
   const int64_t need = (a.n + rows_per_block - 1) / rows_per_block;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)device_props(device).sms * occ));
-  kern<<<grid, 256, 0, s>>>(a);
+  launch_pdl(kern, grid, 256, s, a);
   CSC_LAUNCHED();
   return grid;
 }
@@ -563,7 +595,7 @@ static int launch_typed(const StepArgs& a, int threads, int device, cudaStream_t
     cfg.numAttrs = 1;
     CSC_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   } else {
-    kern<<<grid, threads, 0, s>>>(a);
+    launch_pdl(kern, grid, threads, s, a);
   }
   CSC_LAUNCHED();
   return grid;

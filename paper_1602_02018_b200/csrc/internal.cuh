@@ -79,6 +79,7 @@ struct Options {
   std::atomic<int64_t> lean_mid{1};       // K2: lean mid-step kernel (k_cheb_mid) where it applies
   std::atomic<int64_t> fast_normalize{1}; // K3: vectorised single-panel row normalisation
   std::atomic<int64_t> h2d_overlap{1};    // filters of multi-panel pinned host blocks: per-panel uploads overlap
+  std::atomic<int64_t> pdl{1};            // step kernels launched with programmatic stream serialization (their CSR prologue overlaps the previous step's drain)
   std::atomic<int64_t> l2_policy{1};      // step kernels: output panel stored evict-first (1) or write-back (0)
 };
 extern Options g_opt;

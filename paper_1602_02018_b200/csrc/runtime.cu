@@ -179,6 +179,7 @@ static std::atomic<int64_t>* option_slot(const char* key) {
   if (k == "lean_mid") return &g_opt.lean_mid;
   if (k == "fast_normalize") return &g_opt.fast_normalize;
   if (k == "l2_policy") return &g_opt.l2_policy;
+  if (k == "pdl") return &g_opt.pdl;
   if (k == "h2d_overlap") return &g_opt.h2d_overlap;
   if (k == "block_threads") return &g_opt.block_threads;
   if (k == "profile") return &g_opt.profile;
