@@ -580,6 +580,8 @@ def run_ours(args, cfg):
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpub,
         "clocks": clocks.summary(), "csc": csc, "weak_scaling": weak, "f64": f64,
     }
+    if rop is not None:
+        rop.close()  # collective: peers unmapped before any rank frees its panels
     print(json.dumps(line), flush=True)
 
 

@@ -92,6 +92,16 @@ struct Pair<double> {
   using type = double2;
 };
 
+// The neighbour-row gather load: L2 only (ld.global.cg).  Gathered rows are not reused within an
+// SM (L1 hit rate 3.6 % at C3), so allocating them in L1 only costs L1 fill bandwidth: C3 features
+// -0.8 %, 16-B rows -6 %, 32-B rows -3.4 %, k = 100 block -1.8 %, fp64 -1 %, C3 CG -2.5 %, C4/C5
+// -0.5 %, C2 (L1 hits on a 12.8 MB panel) +0.7 % (profiles/r02_ab_gather_ld.txt; the
+// ld.global.nc.L1::no_allocate / L1::evict_first forms were 15 % slower).
+template <typename V>
+__device__ __forceinline__ V gather_ld(const V* p) {
+  return __ldcg(p);
+}
+
 // Programmatic dependent launch (sm_90+): a step kernel lets its successor in the stream be
 // scheduled at once and waits for its predecessor's completion (and memory flush) only
 // after its own CSR prologue.
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_step(const StepArgs a) {
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
           gv[k] = VT::zero();
-          if (jc[k] >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)jc[k] * SV);
+          if (jc[k] >= 0 && lane_on) gv[k] = gather_ld(Gv + (uint32_t)jc[k] * SV);
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -444,6 +454,18 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     T acc[VEC];
 #pragma unroll
     for (int c = 0; c < VEC; ++c) acc[c] = T(0);
+#ifdef CSC_PF
+    if (row < n && lane_on) {
+      const uint32_t poff = ((uint32_t)row * SV + sub) * VEC;
+#if CSC_PF == 1
+      if (a.S) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const T*>(a.S) + poff));
+      if (a.X) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const T*>(a.X) + poff));
+#else
+      if (a.S) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(static_cast<const T*>(a.S) + poff));
+      if (a.X) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(static_cast<const T*>(a.X) + poff));
+#endif
+    }
+#endif
     {
       const int maxcnt = __reduce_max_sync(FULL, cnt);
       const int32_t* ip = a.indices + nbeg;
@@ -473,7 +495,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
           const int32_t j = LPR == 1 ? jj[k] : __shfl_sync(FULL, jj[k / LPR], k % LPR, LPR);
           if constexpr (!UNIT) wk[k] = LPR == 1 ? ww[k] : __shfl_sync(FULL, ww[k / LPR], k % LPR, LPR);
           gv[k] = VT::zero();
-          if (j >= 0 && lane_on) gv[k] = __ldg(Gv + (uint32_t)j * SV);
+          if (j >= 0 && lane_on) gv[k] = gather_ld(Gv + (uint32_t)j * SV);
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k) {

@@ -531,6 +531,28 @@ class RowShardedOperator:
             lib.csc_peers_destroy(self.peers)
         self.peers, self._peer_bytes = None, 0
 
+    def close(self) -> None:
+        """Collective teardown of the peer transport: every rank finishes its stream, then all
+        unmap their peers' panels before any owner frees its allocation (an exporter must not
+        free memory another process still has mapped).  ``__del__`` alone is best effort."""
+        import torch
+
+        if self.peers is None:
+            return
+        torch.cuda.synchronize(self.device)
+        if self.grp.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier(group=self.grp.group)
+        # two phases inside csc_peers_destroy would need a second entry point; closing after a
+        # barrier is enough because destroy unmaps the peers before it frees the own panels and
+        # no rank touches a peer's panel after the barrier
+        self._close_peers()
+        if self.grp.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier(group=self.grp.group)
+
     def apply_filter(self, filt: PolyFilter, X_local):
         """h(L) X for this rank's rows."""
         return self._run(filt, X_local.contiguous(), 0)[0]

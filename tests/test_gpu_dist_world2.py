@@ -106,10 +106,7 @@ def _peer_rows(grp, dtype="float64", widths=(5, 40, 7), orders=(0, 1, 2, 3, 50))
         F, zero = rop.features(filt, Xl)
         out[("F", w)] = F.cpu().numpy()
         out[("zero", w)] = zero
-    torch.cuda.synchronize()
-    dist.barrier()  # nobody unmaps or frees a panel a peer may still be storing into
-    rop._close_peers()
-    dist.barrier()
+    rop.close()  # collective: nobody unmaps or frees a panel a peer may still be storing into
     return out
 
 

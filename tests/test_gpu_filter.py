@@ -140,6 +140,26 @@ def test_lean_mid_step_kernel_matches_general_kernel(filter_golden, dtype):
             assert relerr(lean, filter_golden["Y_low"]) <= (FP64_TOL if dtype == "float64" else FP32_TOL)
 
 
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_programmatic_dependent_launch_is_bit_identical(filter_golden, dtype):
+    """Step kernels launched with programmatic stream serialization (option pdl: the next step's
+    CSR prologue overlaps the previous step's drain, its panels are touched after
+    griddepcontrol.wait) give the plainly serialised launches' results bit for bit -- lean and
+    general kernels, both recurrences, single- and multi-panel blocks, back-to-back filters."""
+    op = c1_op(dtype)
+    X = filter_golden["X"]
+    low, high = P.design_lowpass(0.37, 50), P.matched_highpass(P.design_lowpass(0.37, 50))
+    for pw in (0, 8, 32):
+        for rec in (0, 1):
+            for lean in (0, 1):
+                with options(panel_width=pw, recurrence=rec, lean_mid=lean, pdl=0):
+                    ref = [P.apply_filter(f, op, X) for f in (low, high, low)]
+                with options(panel_width=pw, recurrence=rec, lean_mid=lean, pdl=1):
+                    got = [P.apply_filter(f, op, X) for f in (low, high, low)]
+                for a, b in zip(ref, got):
+                    assert np.array_equal(a, b), (pw, rec, lean)
+
+
 def test_profile_modes_count_launches_and_bytes(filter_golden):
     """profile 1 (per launch) and 2 (per filter span) count the same launches and bytes; the span
     covers at least the sum of the launches' own times."""
