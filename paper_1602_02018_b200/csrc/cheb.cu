@@ -454,19 +454,6 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     T acc[VEC];
 #pragma unroll
     for (int c = 0; c < VEC; ++c) acc[c] = T(0);
-#ifdef CSC_PF
-    if (row < n && lane_on) {
-      const uint32_t poff = ((uint32_t)row * SV + sub) * VEC;
-#if CSC_PF == 1
-      if (a.S) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const T*>(a.S) + poff));
-      if (a.X) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const T*>(a.X) + poff));
-#else
-      if (a.S) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(static_cast<const T*>(a.S) + poff));
-      if (a.X) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(static_cast<const T*>(a.X) + poff));
-#endif
-    }
-#endif
-    {
       const int maxcnt = __reduce_max_sync(FULL, cnt);
       const int32_t* ip = a.indices + nbeg;
       const T* wp = static_cast<const T*>(a.wv) + nbeg;  // edge weights (weighted graphs only)
