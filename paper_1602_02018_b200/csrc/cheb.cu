@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(256, MINB) k_cheb_mid(const StepArgs a) {
     T acc[VEC];
 #pragma unroll
     for (int c = 0; c < VEC; ++c) acc[c] = T(0);
+    {
       const int maxcnt = __reduce_max_sync(FULL, cnt);
       const int32_t* ip = a.indices + nbeg;
       const T* wp = static_cast<const T*>(a.wv) + nbeg;  // edge weights (weighted graphs only)
