@@ -935,8 +935,9 @@ PanelPlan plan_panels(int64_t n, int w, int dtype, int device, int64_t nnz) {
       // 6.04 -> 7.64 ms) keep one panel (profiles/r02_ab_two_panels.txt)
       const double l2 = (double)device_props(device).l2_bytes;
       const int p128 = 128 / (int)dtype_size(dtype);
-      if (dtype == CSC_F32 && one > p128 && (double)n * one * dtype_size(dtype) > l2 && (double)n * 128.0 <= l2)
-        pw = p128;
+      // (round-2 final kernels, fp64 too: C3 ds = 28 as 16 + 12 columns 23.7 -> 22.3 ms,
+      // gpurun sweep in profiles/r02_plan_sweep_final.txt)
+      if (one > p128 && (double)n * one * dtype_size(dtype) > l2 && (double)n * 128.0 <= l2) pw = p128;
       // ... and in the DRAM-random regime (gather source > 4x L2, C5), where a gathered row
       // costs per 128-B line, a block just over 128 B runs as one 128-B-row panel plus a narrow
       // remainder rather than one 256-B-row panel (C5 probe, 34 columns: 496 -> 401 ms per
