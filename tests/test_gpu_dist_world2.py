@@ -150,3 +150,28 @@ def test_row_sharded_peer_transport_across_processes(world, fn, dtype):
         for p in parts:  # every rank holds the rank-ordered sum of the partials
             assert p[("count", w)] == parts[0][("count", w)]
             assert abs(p[("count", w)] - cref) <= (1e-12 if dtype == "float64" else 1e-5) * cref
+
+
+def test_host_barrier_single_rank_and_failure():
+    """One rank: the host-barrier transport equals the device-barrier one bit for bit, and a
+    failing barrier callback fails the call (CSC_ERR_INVALID -> ValueError) instead of hanging."""
+    import torch
+
+    import paper_1602_02018_b200 as P
+    from paper_1602_02018_b200 import dist as D
+    from gpu_util import c1_op
+
+    g = c1_op().graph
+    X = torch.tensor(np.random.default_rng(0).standard_normal((1000, 9)), dtype=torch.float64, device="cuda")
+    filt = P.design_lowpass(0.6, 20)
+    dev = D.RowShardedOperator(g, D.Group(0, 1), dtype="float64", transport="peer")
+    host = D.RowShardedOperator(g, D.Group(0, 1), dtype="float64", transport="peer", barrier="host")
+    assert torch.equal(dev.apply_filter(filt, X), host.apply_filter(filt, X))
+
+    host._host_barrier = lambda _ctx: 1  # a barrier that reports a lost peer
+    host._barrier_cb = None
+    host._close_peers()
+    with pytest.raises(ValueError, match="host barrier"):
+        host.apply_filter(filt, X)
+    host.close()
+    dev.close()
