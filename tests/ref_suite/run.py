@@ -1,12 +1,13 @@
 """Re-run the reference's own hot-path test modules against the drop-in (TEST INFRASTRUCTURE).
 
     python tests/ref_suite/run.py fetch      # in the build container: copy the modules from
-                                            # /root/reference/pkg/tests into _vendored/ (git-ignored)
+                                            # /root/reference/pkg/tests into oracle/_ref/ref_tests/
+                                            # (git-ignored: the place for reference-derived files)
     python tests/ref_suite/run.py [pytest args]   # on a GPU box: run them, ``cscluster`` -> the drop-in
 
 The modules: test_graph, test_filters, test_spectrum, test_features,
 test_sampling, test_pipeline, test_kmeans, plus their conftest.py / helpers.py.  They are not
-committed (reference sources stay out of the repository); ``_vendored/`` travels to the GPU
+committed (reference sources stay out of the repository); ``oracle/_ref/ref_tests/`` travels to the GPU
 box with the working tree.  Deselected, with the reason:
 """
 
@@ -19,7 +20,7 @@ import sys
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-VENDORED = HERE / "_vendored"
+VENDORED = HERE.parents[1] / "oracle" / "_ref" / "ref_tests"
 SOURCE = Path("/root/reference/pkg/tests")
 MODULES = ("conftest.py", "helpers.py", "test_graph.py", "test_filters.py", "test_spectrum.py",
            "test_features.py", "test_sampling.py", "test_pipeline.py", "test_kmeans.py")
@@ -40,7 +41,7 @@ DESELECT = {
 
 
 def fetch() -> None:
-    VENDORED.mkdir(exist_ok=True)
+    VENDORED.mkdir(parents=True, exist_ok=True)
     for name in MODULES:
         shutil.copyfile(SOURCE / name, VENDORED / name)
     print(f"copied {len(MODULES)} files to {VENDORED}")

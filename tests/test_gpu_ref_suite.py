@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 HERE = Path(__file__).resolve().parent
 
 
-@pytest.mark.skipif(not (HERE / "ref_suite" / "_vendored").exists(),
+@pytest.mark.skipif(not (HERE.parent / "oracle" / "_ref" / "ref_tests").exists(),
                     reason="reference test modules not fetched (tests/ref_suite/run.py fetch)")
 def test_reference_suite_passes_on_the_drop_in():
     out = subprocess.run([sys.executable, str(HERE / "ref_suite" / "run.py"), "-q"], capture_output=True, text=True,
