@@ -99,7 +99,11 @@ struct Pair<double> {
 // ld.global.nc.L1::no_allocate / L1::evict_first forms were 15 % slower).
 template <typename V>
 __device__ __forceinline__ V gather_ld(const V* p) {
+#ifdef CSC_GATHER_NC  // A/B builds only: the read-only path, allocating in L1
+  return __ldg(p);
+#else
   return __ldcg(p);
+#endif
 }
 
 // Programmatic dependent launch (sm_90+): a step kernel lets its successor in the stream be
