@@ -689,21 +689,23 @@ int launch_step(const csc_graph* g, const StepArgs& a_in, int pw, int epi, cudaS
   cudaEvent_t e0 = nullptr;
   if (prof) profile_begin(s, &e0);
   int grid = 0;
-  // Lean mid-step kernel (32 registers, 64 warps/SM) for the hot case: 16-, 64-, 128-, 256- and
-  // 512-B rows whose gather panel is at most 4x L2.  A/B on B200 (profiles/r01_panel_sweeps.txt):
-  // C3 d=56 -1.7 %, CG k=100 -4.7 %, probe d=28 -5.8 %, fp64 d=56 -8.3 %, 16-B rows -4.3 %, 64-B
-  // rows -4.6 %, 512-B rows -4.5 % (C4 k=250) to -20 % (C2 fp64); 32-B rows are 3 % slower and
-  // a 2 GB C5 panel (DRAM-bound random gathers) 3.7 % slower with it: those keep k_cheb_step.
+  // Lean mid-step kernel (32 registers, 64 warps/SM) for the hot case: 16- to 512-B rows whose
+  // gather panel is at most 4x L2 (32-B rows since the final round-2 kernel: C3 8 columns -3.4 %,
+  // C4 -25 %, C2 -6 %, fp64 4 columns -8 % at 6 CTAs/SM, profiles/r02_ab_lean_lpr2.txt).
+  // A/B on B200 (profiles/r01_panel_sweeps.txt): C3 d=56 -1.7 %, CG k=100 -4.7 %, probe d=28
+  // -5.8 %, fp64 d=56 -8.3 %, 16-B rows -4.3 %, 64-B rows -4.6 %, 512-B rows -4.5 % (C4 k=250) to
+  // -20 % (C2 fp64); a 2 GB C5 panel (DRAM-bound random gathers) is 3.7 % slower with it and
+  // keeps k_cheb_step.
   // Weighted graphs: fp32 -3.5 to -5 %, fp64 +5 % (weights cost the fp64 build its buffers).
   const bool lean = g_opt.lean_mid.load() != 0 && epi == EPI_NONE && (a.wv == nullptr || sizeof(T) == 4) &&
                     !a.fwd && !a.last &&
                     a.npeers == 0 && a.G != nullptr && a.O != nullptr && !a.contig && threads == 256 &&
                     g_opt.unroll.load() == 4 && g_opt.persistent.load() && persist_bytes(g->device) == 0 &&
-                    lpr != 2 &&
                     (double)gsrc * a.sv * 16.0 <= 4.0 * (double)device_props(g->device).l2_bytes;
   if (lean) {
     switch (lpr) {
       case 1: grid = launch_mid<T, 1>(a, g->device, s); break;
+      case 2: grid = launch_mid<T, 2>(a, g->device, s); break;
       case 4: grid = launch_mid<T, 4>(a, g->device, s); break;
       case 8: grid = launch_mid<T, 8>(a, g->device, s); break;
       case 16: grid = launch_mid<T, 16>(a, g->device, s); break;

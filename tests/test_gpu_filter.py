@@ -130,7 +130,7 @@ def test_lean_mid_step_kernel_matches_general_kernel(filter_golden, dtype):
     op = c1_op(dtype)
     X = filter_golden["X"]
     low = P.design_lowpass(0.37, 50)
-    for pw in (0, 8, 16, 32, 64):
+    for pw in (0, 4, 8, 16, 32, 64):
         for rec in (0, 1):
             with options(panel_width=pw, recurrence=rec, lean_mid=0):
                 general = P.apply_filter(low, op, X)
