@@ -24,6 +24,8 @@ from paper_1602_02018_b200.pipeline import CscParams
 from paper_1602_02018_b200.sampling import CgInfo
 from paper_1602_02018_b200.sbm import sbm_edges
 
+pytestmark = pytest.mark.timeout(900)  # a lost rank must fail the run, not hang it
+
 
 class OracleBackend:
     """CPU per-rank compute for the tests (the product uses dist.DeviceBackend)."""

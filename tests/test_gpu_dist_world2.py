@@ -16,7 +16,8 @@ import pytest
 from conftest import D_C1
 from test_dist_gloo import run_world
 
-pytestmark = pytest.mark.gpu
+# a lost rank must fail the run, not hang it (pytest-timeout; the spawn helper also tears the world down)
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
 
 
 def _device_run(grp):
