@@ -71,9 +71,16 @@ int csc_launch_count(int64_t* out);
  *   "unroll"        neighbour gathers in flight per lane / occupancy: 4 (default: 4 in
  *                   flight, 6 CTAs/SM), 2 (4 in flight, 8 CTAs/SM), 8 (8 in flight, 2 CTAs/SM)
  *   "row_order"     0 interleaved row groups (default), 1 contiguous runs per warp
- *   "lean_mid"      1 (default): lean mid-step kernel for 16/64/128/256/512-B panel rows whose
+ *   "lean_mid"      1 (default): lean mid-step kernel for 16- to 512-B panel rows whose
  *                   gather panel is <= 4x L2 (unit weights; weighted graphs in fp32);
  *                   0: always the general step kernel
+ *   "pdl"           1 (default): step kernels are launched with programmatic stream
+ *                   serialization (their CSR prologue overlaps the previous step's drain); 0 off
+ *   "l2_policy"     1 (default): a step's output panel is stored evict-first; 0 write-back
+ *   "persistent"    1 (default): step grids of resident CTAs (grid-stride); 0 one CTA per row block
+ *   "fast_normalize" 1 (default): vectorised row normaliser for equal-width panels
+ *   "h2d_overlap"   1 (default): multi-panel pinned host blocks upload panel by panel,
+ *                   overlapping the earlier panels' filters
  *   "l2_budget_pct" L2 share a gathered panel may use (auto panel width)
  *   "l2_persist_pct" >0: persisting-L2 access window on the gathered panel
  *   "cg_compact"    1 (default): block CG moves still-active columns into narrower panels
