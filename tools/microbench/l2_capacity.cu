@@ -4,7 +4,7 @@
 //   ncu --metrics dram__bytes_read.sum,lts__t_sector_hit_rate.pct,gpu__time_duration.sum --clock-control none
 // to read the DRAM bytes per pass: with G gathers of 128 B over a source of S bytes, a cache that
 // holds C bytes of it reads about S + (1 - C/S) * 128 G from DRAM once warm.
-//   l2_capacity [gathers_in_millions]
+//   l2_capacity [gathers_in_millions] [mode: 0 all SMs, 1 smid < half, 2 even smid, 3 smid >= half]
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2_capacity l2_capacity.cu
 #include <cuda_runtime.h>
 
@@ -28,6 +28,45 @@ __device__ __forceinline__ uint32_t mix(uint32_t x) {
   x *= 0x846ca68bu;
   x ^= x >> 16;
   return x;
+}
+
+// mode 0: every SM gathers; 1: SMs with %smid < half only; 2: SMs with even %smid only
+// (the participating CTAs split the same number of gathers among themselves through a counter)
+__device__ unsigned long long g_next;
+
+__global__ void __launch_bounds__(256, 8) k_gather_sel(const float4* __restrict__ G, uint32_t rows, long gathers,
+                                                       uint32_t salt, float* __restrict__ sink, int mode, int half) {
+  unsigned smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (mode == 1 && (int)smid >= half) return;
+  if (mode == 2 && (smid & 1)) return;
+  if (mode == 3 && (int)smid < half) return;
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (;;) {
+    unsigned long long e0 = 0;
+    if (lane == 0) e0 = atomicAdd(&g_next, 256ull);
+    e0 = __shfl_sync(0xffffffffu, e0, 0);
+    if ((long)e0 >= gathers) break;
+#pragma unroll 4
+    for (int r = 0; r < 16; ++r) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t e = (uint32_t)(e0 + r * 16 + u * 4 + grp);
+        const uint32_t j = (uint32_t)(((uint64_t)mix(e ^ salt) * rows) >> 32);
+        v[u] = __ldcg(G + (size_t)j * 8 + sub);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+  }
+  if (acc.x + acc.y + acc.z + acc.w == 12345.f) sink[0] = acc.x;
 }
 
 __global__ void __launch_bounds__(256, 8) k_gather(const float4* __restrict__ G, uint32_t rows, long gathers,
@@ -57,10 +96,11 @@ __global__ void __launch_bounds__(256, 8) k_gather(const float4* __restrict__ G,
 
 int main(int argc, char** argv) {
   const long gathers = (argc > 1 ? atol(argv[1]) : 16) * 1000000L;
+  const int mode = argc > 2 ? atoi(argv[2]) : 0;  // SM subset (see k_gather_sel)
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, 0));
-  printf("%s, %d SMs, L2 %.1f MiB; %ld gathers of 128 B per pass\n", prop.name, prop.multiProcessorCount,
-         prop.l2CacheSize / 1048576.0, gathers);
+  printf("%s, %d SMs, L2 %.1f MiB; %ld gathers of 128 B per pass; SM subset mode %d\n", prop.name,
+         prop.multiProcessorCount, prop.l2CacheSize / 1048576.0, gathers, mode);
   float* sink;
   CK(cudaMalloc(&sink, 4));
   const int sizes_mb[] = {16, 32, 48, 56, 64, 72, 80, 96, 112, 128, 160, 192, 256};
@@ -76,7 +116,13 @@ int main(int argc, char** argv) {
     const int grid = prop.multiProcessorCount * 8;
     for (int pass = 0; pass < 3; ++pass) {  // pass 0 warms; passes 1 and 2 use fresh index sequences
       CK(cudaEventRecord(e0));
-      k_gather<<<grid, 256>>>(G, rows, gathers, 0x9e3779b9u * (pass + 1), sink);
+      if (mode == 0) {
+        k_gather<<<grid, 256>>>(G, rows, gathers, 0x9e3779b9u * (pass + 1), sink);
+      } else {
+        unsigned long long zero = 0;
+        CK(cudaMemcpyToSymbol(g_next, &zero, sizeof(zero)));
+        k_gather_sel<<<grid, 256>>>(G, rows, gathers, 0x9e3779b9u * (pass + 1), sink, mode, prop.multiProcessorCount / 2);
+      }
       CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1));
       float ms;
